@@ -1,0 +1,77 @@
+"""Host <-> device conversion for the reference-compatible list API.
+
+Keys and values travel as integer tensors holding the table's storage bit
+pattern (int32 for <= 32-bit fields, int64 otherwise; uint64 keys >= 2^63
+simply appear negative in the int64 view).  CUDA tensors are used in place;
+Python sequences and numpy arrays are staged through pinned host memory.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+def torch_dtype(bits: int) -> torch.dtype:
+    return torch.int32 if bits <= 32 else torch.int64
+
+
+def np_dtype(bits: int):
+    return np.uint32 if bits <= 32 else np.uint64
+
+
+def _np_signed(bits: int):
+    return np.int32 if bits <= 32 else np.int64
+
+
+def to_numpy(seq, bits: int, what: str = "key") -> np.ndarray:
+    """Python ints / arrays -> contiguous unsigned array of the storage width."""
+    if isinstance(seq, np.ndarray):
+        arr = seq
+        if arr.dtype.kind == "i" and arr.size and arr.min() < 0:
+            raise ValueError(f"negative {what}")
+        arr = arr.astype(np.uint64, copy=False)
+    else:
+        seq = list(seq)
+        try:
+            arr = np.array(seq, dtype=np.uint64) if seq else np.empty(0, dtype=np.uint64)
+        except (OverflowError, ValueError, TypeError) as err:
+            raise ValueError(f"{what}s must be integers in [0, 2^64)") from err
+    if bits <= 32:
+        if arr.size and arr.max() > np.uint64(0xFFFFFFFF):
+            raise ValueError(f"{what} does not fit in {bits} bits")
+        arr = arr.astype(np.uint32)
+    return np.ascontiguousarray(arr)
+
+
+def to_device(x, bits: int, device: int, what: str = "key") -> torch.Tensor:
+    """Anything array-like -> contiguous CUDA tensor of the storage width."""
+    dt = torch_dtype(bits)
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda and x.dtype == dt and x.is_contiguous() and x.device.index == device:
+            return x
+        if x.dtype in (torch.int32, torch.int64, torch.uint32, torch.uint64) and x.element_size() == \
+                torch.tensor([], dtype=dt).element_size():
+            return x.contiguous().view(dt).to(f"cuda:{device}", non_blocking=True)
+        x = x.cpu().numpy()
+    arr = to_numpy(x, bits, what)
+    host = torch.from_numpy(arr.view(_np_signed(bits)))
+    if host.numel() > (1 << 16):
+        host = host.pin_memory()
+    return host.to(f"cuda:{device}", non_blocking=True)
+
+
+def from_device(t: torch.Tensor, bits: int) -> np.ndarray:
+    """CUDA integer tensor -> unsigned numpy array (bit-exact)."""
+    a = t.cpu().numpy()
+    return a.view(np.uint32 if a.dtype.itemsize == 4 else np.uint64)
+
+
+def stream_of(device: int, stream=None) -> int:
+    if stream is None:
+        return torch.cuda.current_stream(device).cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def split_pairs(pairs) -> tuple[list, list]:
+    pairs = list(pairs)
+    return [k for k, _ in pairs], [v for _, v in pairs]

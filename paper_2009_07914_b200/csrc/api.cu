@@ -1,0 +1,674 @@
+// api.cu -- the extern "C" boundary (include/coophash_b200.h).
+//
+// Owns table memory (cudaMalloc), orders every operation on a table after the
+// previous one (a per-table event), validates configurations the way the
+// reference constructors do, and turns CUDA errors into negative codes with a
+// thread-local message.  No exception crosses the ABI.
+#include <cerrno>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/coophash_b200.h"
+#include "bucket.cuh"
+#include "dispatch.cuh"
+
+namespace chb {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+// prims.cu / bucket.cu entry points
+int mix64_array(const Launch& lc, const uint64_t* in, uint64_t n, uint64_t seed, uint64_t* out);
+int multi_split(const Launch& lc, const void* keys, int kbytes, const void* vals, int vbytes, uint64_t n,
+                uint32_t shards, uint64_t* perm, uint64_t* offsets, void* keys_out, void* vals_out, void* scratch,
+                size_t scratch_bytes);
+size_t split_scratch_bytes(uint64_t n, uint32_t shards);
+int permute(const Launch& lc, const void* src, int elem_bytes, const uint64_t* perm, uint64_t n, void* dst,
+            bool scatter);
+int segment_copy(const Launch& lc, const void* src, int elem_bytes, const uint64_t* src_off, const uint64_t* idx,
+                 uint64_t n, const uint64_t* dst_off, void* dst);
+
+int bucket_insert(const Launch& lc, const BucketRef& B, const TypeSel& ts, const void* keys, const void* vals,
+                  uint64_t n, uint8_t* status, int64_t* slots, uint32_t* rank, uint64_t* need, uint64_t* alloc_off,
+                  void* scan_scratch, size_t scan_bytes);
+int bucket_counts(const Launch& lc, const uint64_t* handles, uint64_t n, uint32_t* counts);
+int bucket_walk(const Launch& lc, const BucketRef& B, int vbytes, const uint64_t* handles, uint64_t n,
+                const uint64_t* offsets, void* out);
+
+}  // namespace chb
+
+using namespace chb;
+
+struct ch_table {
+  ch_config cfg;
+  TypeSel ts;          // storage types of the slot array
+  TableRef T;
+  int kbytes, vbytes;  // user-visible value width (bucket: arena value width)
+  size_t slot_bytes = 0, val_bytes = 0;
+  DevCounters* ctr = nullptr;
+  uint64_t host_ops = 0;  // ops accounted on the host (count passes)
+  // bucket list
+  void* arena = nullptr;
+  unsigned long long* bump = nullptr;  // also holds first_fail at [1]
+  uint32_t* bcnt = nullptr;
+  BucketInfo* info = nullptr;
+  uint64_t* gsizes = nullptr;
+  uint64_t* gsums = nullptr;
+  uint64_t gm = 0;
+  cudaEvent_t last = nullptr;
+  std::mutex mu;
+  int sms = 148;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+int check(cudaError_t e, const char* what) { return cuda_check(e, what); }
+
+// Every op on a table runs after the previous one, on the caller's stream.
+struct Ordered {
+  ch_table* t;
+  cudaStream_t s;
+  Launch lc;
+  std::lock_guard<std::mutex> lock;
+  DeviceGuard dev;
+  Ordered(ch_table* t_, void* stream) : t(t_), s((cudaStream_t)stream), lock(t_->mu), dev(t_->cfg.device) {
+    lc.stream = s;
+    lc.device = t->cfg.device;
+    lc.sms = t->sms;
+    cudaStreamWaitEvent(s, t->last, 0);
+  }
+  int done(int rc) {
+    cudaError_t e = cudaEventRecord(t->last, s);
+    if (rc) return rc;
+    return check(e, "event record");
+  }
+};
+
+struct Scratch {  // stream-ordered transient device memory
+  cudaStream_t s;
+  std::vector<void*> bufs;
+  explicit Scratch(cudaStream_t s_) : s(s_) {}
+  void* get(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes ? bytes : 8, s) != cudaSuccess) return nullptr;
+    bufs.push_back(p);
+    return p;
+  }
+  ~Scratch() {
+    for (void* p : bufs) cudaFreeAsync(p, s);
+  }
+};
+
+bool pow2_group(int g) { return g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32; }
+
+// exact growth sizes: s_i = ceil(num/den * s_{i-1}) until the sums cover COUNT_MAX
+bool growth_table(uint64_t s0, uint64_t num, uint64_t den, std::vector<uint64_t>& sizes, std::vector<uint64_t>& sums) {
+  const uint64_t count_max = (1ull << 20) - 1;
+  uint64_t s = s0, acc = 0;
+  while (acc < count_max) {
+    sizes.push_back(s);
+    acc += s;
+    sums.push_back(acc);
+    unsigned __int128 nx = ((unsigned __int128)s * num + den - 1) / den;
+    if (nx > ((unsigned __int128)1 << 62)) nx = (unsigned __int128)1 << 62;
+    s = (uint64_t)nx;
+  }
+  return true;
+}
+
+BucketRef bucket_ref(ch_table* t) {
+  BucketRef B;
+  B.T = t->T;
+  B.arena = t->arena;
+  B.pool_cap = t->cfg.pool_capacity;
+  B.bump = t->bump;
+  B.bcnt = t->bcnt;
+  B.info = t->info;
+  B.first_fail = t->bump + 1;
+  B.gr.sizes = t->gsizes;
+  B.gr.sums = t->gsums;
+  B.gr.m = t->gm;
+  return B;
+}
+
+__global__ void k_zero_counters(DevCounters* c) { *c = DevCounters{}; }
+
+__global__ void k_reset_probe(DevCounters* c) {
+  c->ops = 0;
+  c->attempts = 0;
+  c->windows = 0;
+}
+
+// element transitions of layout.py:140-243 on one slot
+template <typename K, typename V>
+__global__ void k_slot_op(TableRef T, int layout, int op, uint64_t slot, uint64_t expected, uint64_t desired,
+                          uint64_t value, unsigned long long* out) {
+  const K e = (K)T.e, t = (K)T.t;
+  int w = 0;
+  uint64_t seen_k = 0, seen_v = 0;
+  if (layout == PACKED) {
+    unsigned long long* p = static_cast<unsigned long long*>(T.slots) + slot;
+    unsigned long long cur = *p;
+    for (;;) {
+      const uint32_t k = (uint32_t)cur;
+      unsigned long long nxt = cur;
+      bool apply = false;
+      if (op == 0) { apply = k == (uint32_t)expected; nxt = (cur & ~0xFFFFFFFFull) | (uint32_t)desired; }
+      else if (op == 1) { apply = k == (uint32_t)e || k == (uint32_t)t; nxt = (value << 32) | (uint32_t)desired; }
+      else if (op == 3) { apply = k == (uint32_t)expected; nxt = (value << 32) | (uint32_t)t; }
+      else if (op == 4) { apply = true; nxt = (value << 32) | k; }
+      seen_k = k;
+      seen_v = cur >> 32;
+      if (!apply) break;
+      const unsigned long long prev = atomicCAS(p, cur, nxt);
+      if (prev == cur) { w = 1; break; }
+      cur = prev;
+    }
+  } else {
+    K* kp;
+    V* vp;
+    if (layout == SOA) { kp = static_cast<K*>(T.slots) + slot; vp = static_cast<V*>(T.vals) + slot; }
+    else { auto* c = static_cast<CellT<K, V>*>(T.slots) + slot; kp = &c->k; vp = &c->v; }
+    seen_k = *(volatile K*)kp;
+    seen_v = *(volatile V*)vp;
+    if (op == 0 || op == 3) {
+      const K des = op == 0 ? (K)desired : t;
+      const K prev = atomic_cas(kp, (K)expected, des);
+      w = prev == (K)expected;
+      seen_k = prev;
+    } else if (op == 2) {
+      const V prev = atomic_cas(vp, (V)expected, (V)desired);
+      w = prev == (V)expected;
+      seen_v = prev;
+    } else if (op == 4) {
+      *vp = (V)value;
+      w = 1;
+    } else if (op == 5) {
+      w = 1;
+    }
+  }
+  out[0] = (unsigned long long)w;
+  out[1] = seen_k;
+  out[2] = seen_v;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ch_last_error(void) { return g_err.c_str(); }
+int ch_version(void) { return 1; }
+
+int ch_create(ch_table** out, const ch_config* cfg) {
+  if (!out || !cfg) return fail(CH_EINVAL, "null argument");
+  *out = nullptr;
+  const ch_config& c = *cfg;
+  if (c.kind < CH_SINGLE || c.kind > CH_BUCKET) return fail(CH_EINVAL, "bad table kind");
+  if (c.layout < CH_SOA || c.layout > CH_PACKED) return fail(CH_EINVAL, "bad layout");
+  if (c.key_bits < 1 || c.key_bits > 64 || c.value_bits < 1 || c.value_bits > 64)
+    return fail(CH_EINVAL, "key_bits / value_bits must be in [1, 64]");
+  if (c.layout == CH_PACKED && (c.key_bits > 32 || c.value_bits > 32))
+    return fail(CH_EINVAL, "packed layout needs 32-bit keys and values");
+  if (c.kind == CH_BUCKET && c.layout == CH_PACKED)
+    return fail(CH_EINVAL, "list handles need 64-bit value cells; use the soa or aos layout");
+  if (!pow2_group(c.group_width)) return fail(CH_EINVAL, "group_width must be one of (1, 2, 4, 8, 16, 32)");
+  if (c.p < 2) return fail(CH_EINVAL, "window count p must be a prime >= 2");
+  const uint64_t maxw = c.max_outer_attempts ? c.max_outer_attempts : c.p;
+  if (maxw < 1 || maxw > c.p) return fail(CH_EINVAL, "max_outer_attempts must be in [1, p]");
+  if (c.empty_key == c.tombstone_key) return fail(CH_EINVAL, "empty and tombstone sentinels must differ");
+  const int kbytes = c.key_bits <= 32 ? 4 : 8;
+  const int vbytes = c.value_bits <= 32 ? 4 : 8;
+  if (kbytes == 4 && (c.empty_key > 0xFFFFFFFFull || c.tombstone_key > 0xFFFFFFFFull))
+    return fail(CH_EINVAL, "sentinels do not fit the key width");
+  if (c.kind == CH_BUCKET) {
+    if (c.pool_capacity == 0) return fail(CH_EINVAL, "pool capacity must be positive");
+    if (c.growth_s0 < 1) return fail(CH_EINVAL, "initial bucket size must be >= 1");
+    if (c.growth_den == 0 || c.growth_num < c.growth_den) return fail(CH_EINVAL, "growth factor must be >= 1");
+    if (vbytes == 4 && c.pool_capacity > 0xFFFFFFFFull)
+      return fail(CH_EINVAL, "32-bit value arenas hold at most 2^32-1 cells");
+    if (c.pool_capacity > (1ull << 42) - 1) return fail(CH_EINVAL, "pool capacity exceeds the 42-bit tail");
+  }
+  DeviceGuard dev(c.device);
+  if (!dev.ok) return fail(CH_EINVAL, "bad device ordinal");
+
+  ch_table* t = new (std::nothrow) ch_table();
+  if (!t) return fail(CH_ENOMEM, "host allocation failed");
+  t->cfg = c;
+  t->cfg.max_outer_attempts = maxw;
+  t->kbytes = kbytes;
+  t->vbytes = vbytes;
+  t->ts.layout = c.layout;
+  t->ts.kbytes = kbytes;
+  t->ts.vbytes = c.kind == CH_BUCKET ? 8 : vbytes;
+  t->ts.g = c.group_width;
+  cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, c.device);
+
+  const uint64_t cap = 32 * c.p;
+  TableRef& T = t->T;
+  T.c = cap;
+  T.p = c.p;
+  T.max_windows = maxw;
+  T.e = c.empty_key;
+  T.t = c.tombstone_key;
+  T.modc = FastMod::make(cap);
+  T.modpm1 = FastMod::make(c.p - 1);
+  T.slots = T.vals = nullptr;
+
+  auto cleanup = [&](int code, const std::string& msg) {
+    ch_destroy(t);
+    return fail(code, msg);
+  };
+  if (cudaEventCreateWithFlags(&t->last, cudaEventDisableTiming) != cudaSuccess)
+    return cleanup(CH_EIO, "event create failed");
+  const int sv = t->ts.vbytes;
+  if (c.layout == CH_PACKED) t->slot_bytes = cap * 8;
+  else if (c.layout == CH_SOA) { t->slot_bytes = cap * kbytes; t->val_bytes = cap * sv; }
+  else t->slot_bytes = cap * (size_t)(kbytes == 8 || sv == 8 ? 16 : 8);
+  if (cudaMalloc(&T.slots, t->slot_bytes) != cudaSuccess) return cleanup(CH_ENOMEM, "slot array allocation failed");
+  if (t->val_bytes && cudaMalloc(&T.vals, t->val_bytes) != cudaSuccess)
+    return cleanup(CH_ENOMEM, "value array allocation failed");
+  if (cudaMalloc(&t->ctr, sizeof(DevCounters)) != cudaSuccess) return cleanup(CH_ENOMEM, "counter allocation failed");
+  T.ctr = t->ctr;
+
+  if (c.kind == CH_BUCKET) {
+    std::vector<uint64_t> sizes, sums;
+    growth_table(c.growth_s0, c.growth_num, c.growth_den, sizes, sums);
+    t->gm = sizes.size();
+    if (cudaMalloc(&t->arena, c.pool_capacity * vbytes) != cudaSuccess) return cleanup(CH_ENOMEM, "arena allocation failed");
+    if (cudaMalloc(&t->bump, 2 * sizeof(unsigned long long)) != cudaSuccess) return cleanup(CH_ENOMEM, "bump alloc");
+    if (cudaMalloc(&t->bcnt, cap * sizeof(uint32_t)) != cudaSuccess) return cleanup(CH_ENOMEM, "batch count alloc");
+    if (cudaMalloc(&t->info, cap * sizeof(BucketInfo)) != cudaSuccess) return cleanup(CH_ENOMEM, "bucket info alloc");
+    if (cudaMalloc(&t->gsizes, t->gm * 8) != cudaSuccess || cudaMalloc(&t->gsums, t->gm * 8) != cudaSuccess)
+      return cleanup(CH_ENOMEM, "growth table alloc");
+    if (cudaMemcpy(t->gsizes, sizes.data(), t->gm * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(t->gsums, sums.data(), t->gm * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+      return cleanup(CH_EIO, "growth table upload failed");
+  }
+  int rc = ch_clear(t, nullptr);
+  if (rc) {
+    std::string m = g_err;
+    return cleanup(rc, m);
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(CH_EIO, "table init failed");
+  *out = t;
+  return CH_OK;
+}
+
+int ch_destroy(ch_table* t) {
+  if (!t) return CH_OK;
+  DeviceGuard dev(t->cfg.device);
+  if (t->last) cudaEventSynchronize(t->last);
+  cudaFree(t->T.slots);
+  cudaFree(t->T.vals);
+  cudaFree(t->ctr);
+  cudaFree(t->arena);
+  cudaFree(t->bump);
+  cudaFree(t->bcnt);
+  cudaFree(t->info);
+  cudaFree(t->gsizes);
+  cudaFree(t->gsums);
+  if (t->last) cudaEventDestroy(t->last);
+  delete t;
+  return CH_OK;
+}
+
+int ch_clear(ch_table* t, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  Ordered o(t, stream);
+  int rc = single_clear(o.lc, t->T, t->ts);
+  if (!rc) {
+    k_zero_counters<<<1, 1, 0, o.s>>>(t->ctr);
+    rc = check(cudaGetLastError(), "zero counters");
+  }
+  if (!rc && t->cfg.kind == CH_BUCKET) {
+    rc = check(cudaMemsetAsync(t->bump, 0, 2 * sizeof(unsigned long long), o.s), "bump reset");
+    if (!rc) rc = check(cudaMemsetAsync(t->bcnt, 0, t->T.c * sizeof(uint32_t), o.s), "batch count reset");
+    if (!rc) rc = check(cudaMemsetAsync(t->arena, 0, t->cfg.pool_capacity * t->vbytes, o.s), "arena reset");
+  }
+  t->host_ops = 0;
+  return o.done(rc);
+}
+
+int ch_synchronize(ch_table* t) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  DeviceGuard dev(t->cfg.device);
+  return check(cudaEventSynchronize(t->last), "synchronize");
+}
+
+int ch_get_stats(ch_table* t, ch_stats* out) {
+  if (!t || !out) return fail(CH_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard dev(t->cfg.device);
+  int rc = check(cudaEventSynchronize(t->last), "synchronize");
+  if (rc) return rc;
+  DevCounters c;
+  rc = check(cudaMemcpy(&c, t->ctr, sizeof(c), cudaMemcpyDeviceToHost), "read counters");
+  if (rc) return rc;
+  out->capacity = t->T.c;
+  out->occupied = c.occupied;
+  out->tombstones = c.tombstones;
+  out->ops = c.ops + t->host_ops;
+  out->attempts = c.attempts;
+  out->windows = c.windows;
+  out->total_values = c.total_values;
+  out->pool_allocated = c.pool_used;
+  out->device_error = c.error;
+  return CH_OK;
+}
+
+int ch_reset_probe_counters(ch_table* t, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  Ordered o(t, stream);
+  k_reset_probe<<<1, 1, 0, o.s>>>(t->ctr);
+  t->host_ops = 0;
+  return o.done(check(cudaGetLastError(), "reset counters"));
+}
+
+int ch_insert(ch_table* t, const void* keys, const void* vals, uint64_t n, uint8_t* status, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (t->cfg.kind != CH_SINGLE) return fail(CH_EINVAL, "ch_insert needs a single-value table");
+  if (n && (!keys || !vals || !status)) return fail(CH_EINVAL, "null buffer");
+  Ordered o(t, stream);
+  return o.done(single_insert(o.lc, t->T, t->ts, keys, vals, n, status, nullptr, 0));
+}
+
+int ch_find_or_claim(ch_table* t, const void* keys, uint64_t n, uint8_t* status, int64_t* slots, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (t->cfg.kind == CH_MULTI) return fail(CH_EINVAL, "find_or_claim needs a single-value or bucket table");
+  if (n && (!keys || !status || !slots)) return fail(CH_EINVAL, "null buffer");
+  Ordered o(t, stream);
+  return o.done(single_insert(o.lc, t->T, t->ts, keys, nullptr, n, status, slots, 1));
+}
+
+int ch_retrieve(ch_table* t, const void* keys, uint64_t n, void* vals_out, uint8_t* found, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (t->cfg.kind != CH_SINGLE) return fail(CH_EINVAL, "ch_retrieve needs a single-value table");
+  if (n && (!keys || !vals_out || !found)) return fail(CH_EINVAL, "null buffer");
+  Ordered o(t, stream);
+  return o.done(single_lookup(o.lc, t->T, t->ts, keys, n, vals_out, found, nullptr, nullptr, nullptr, 0));
+}
+
+int ch_erase(ch_table* t, const void* keys, uint64_t n, uint8_t* erased, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (t->cfg.kind != CH_SINGLE) return fail(CH_EINVAL, "erase is only defined for single-value tables");
+  if (n && (!keys || !erased)) return fail(CH_EINVAL, "null buffer");
+  Ordered o(t, stream);
+  return o.done(single_lookup(o.lc, t->T, t->ts, keys, n, nullptr, erased, nullptr, nullptr, nullptr, 2));
+}
+
+int ch_find(ch_table* t, const void* keys, uint64_t n, int64_t* slots, uint32_t* attempts, uint32_t* windows,
+            void* vals_out, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (n && (!keys || !slots)) return fail(CH_EINVAL, "null buffer");
+  Ordered o(t, stream);
+  return o.done(single_lookup(o.lc, t->T, t->ts, keys, n, vals_out, nullptr, slots, attempts, windows, 1));
+}
+
+int ch_multi_insert(ch_table* t, const void* keys, const void* vals, uint64_t n, uint8_t* status, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (t->cfg.kind != CH_MULTI) return fail(CH_EINVAL, "ch_multi_insert needs a multi-value table");
+  if (n && (!keys || !vals || !status)) return fail(CH_EINVAL, "null buffer");
+  Ordered o(t, stream);
+  return o.done(multi_insert(o.lc, t->T, t->ts, keys, vals, n, status));
+}
+
+int ch_multi_count(ch_table* t, const void* keys, uint64_t n, uint32_t* counts, uint64_t* offsets, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (t->cfg.kind != CH_MULTI) return fail(CH_EINVAL, "ch_multi_count needs a multi-value table");
+  if (!offsets || (n && (!keys || !counts))) return fail(CH_EINVAL, "null buffer");
+  Ordered o(t, stream);
+  Scratch sc(o.s);
+  int rc = multi_scan(o.lc, t->T, t->ts, keys, n, counts, nullptr, nullptr, 0);
+  if (!rc) {
+    const size_t sb = exclusive_scan_scratch_bytes(n);
+    void* p = sc.get(sb);
+    rc = p ? exclusive_scan_u32(o.lc, counts, n, offsets, p, sb) : fail(CH_ENOMEM, "scratch allocation failed");
+  }
+  t->host_ops += n;
+  return o.done(rc);
+}
+
+int ch_multi_retrieve(ch_table* t, const void* keys, uint64_t n, const uint64_t* offsets, void* vals_out,
+                      void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (t->cfg.kind != CH_MULTI) return fail(CH_EINVAL, "ch_multi_retrieve needs a multi-value table");
+  if (n && (!keys || !offsets)) return fail(CH_EINVAL, "null buffer");
+  Ordered o(t, stream);
+  t->host_ops += n;
+  return o.done(multi_scan(o.lc, t->T, t->ts, keys, n, nullptr, offsets, vals_out, 1));
+}
+
+int ch_bucket_insert(ch_table* t, const void* keys, const void* vals, uint64_t n, uint8_t* status, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (t->cfg.kind != CH_BUCKET) return fail(CH_EINVAL, "ch_bucket_insert needs a bucket-list table");
+  if (n && (!keys || !vals || !status)) return fail(CH_EINVAL, "null buffer");
+  if (n == 0) return CH_OK;
+  Ordered o(t, stream);
+  Scratch sc(o.s);
+  const uint64_t c = t->T.c;
+  const size_t sb = exclusive_scan_scratch_bytes(c + 1);
+  int64_t* slots = (int64_t*)sc.get(n * 8);
+  uint32_t* rank = (uint32_t*)sc.get(n * 4);
+  uint64_t* need = (uint64_t*)sc.get(c * 8);
+  uint64_t* alloc_off = (uint64_t*)sc.get((c + 1) * 8);
+  void* scan = sc.get(sb);
+  if (!slots || !rank || !need || !alloc_off || !scan) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+  TypeSel ts = t->ts;
+  ts.vbytes = t->vbytes;  // arena value width for the write pass
+  return o.done(bucket_insert(o.lc, bucket_ref(t), ts, keys, vals, n, status, slots, rank, need, alloc_off, scan, sb));
+}
+
+int ch_bucket_count(ch_table* t, const void* keys, uint64_t n, uint32_t* counts, uint64_t* offsets,
+                    uint64_t* handles, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (t->cfg.kind != CH_BUCKET) return fail(CH_EINVAL, "ch_bucket_count needs a bucket-list table");
+  if (!offsets || (n && (!keys || !counts || !handles))) return fail(CH_EINVAL, "null buffer");
+  Ordered o(t, stream);
+  Scratch sc(o.s);
+  uint8_t* found = (uint8_t*)sc.get(n);
+  const size_t sb = exclusive_scan_scratch_bytes(n);
+  void* scan = sc.get(sb);
+  if (!found || !scan) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+  int rc = single_lookup(o.lc, t->T, t->ts, keys, n, handles, found, nullptr, nullptr, nullptr, 0);
+  if (!rc) rc = bucket_counts(o.lc, handles, n, counts);
+  if (!rc) rc = exclusive_scan_u32(o.lc, counts, n, offsets, scan, sb);
+  return o.done(rc);
+}
+
+int ch_bucket_retrieve(ch_table* t, const uint64_t* handles, uint64_t n, const uint64_t* offsets, void* vals_out,
+                       void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (t->cfg.kind != CH_BUCKET) return fail(CH_EINVAL, "ch_bucket_retrieve needs a bucket-list table");
+  if (n && (!handles || !offsets)) return fail(CH_EINVAL, "null buffer");
+  Ordered o(t, stream);
+  return o.done(bucket_walk(o.lc, bucket_ref(t), t->vbytes, handles, n, offsets, vals_out));
+}
+
+int ch_read_slots(ch_table* t, void* h_keys, void* h_vals) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard dev(t->cfg.device);
+  int rc = check(cudaEventSynchronize(t->last), "synchronize");
+  if (rc) return rc;
+  const uint64_t c = t->T.c;
+  const int kb = t->ts.kbytes, vb = t->ts.vbytes;
+  if (t->cfg.layout == CH_SOA) {
+    if (h_keys) rc = check(cudaMemcpy(h_keys, t->T.slots, c * kb, cudaMemcpyDeviceToHost), "read keys");
+    if (!rc && h_vals) rc = check(cudaMemcpy(h_vals, t->T.vals, c * vb, cudaMemcpyDeviceToHost), "read values");
+    return rc;
+  }
+  const size_t cell = t->cfg.layout == CH_PACKED ? 8 : (kb == 8 || vb == 8 ? 16 : 8);
+  std::vector<unsigned char> buf;
+  try {
+    buf.resize(c * cell);
+  } catch (...) {
+    return fail(CH_ENOMEM, "host buffer");
+  }
+  rc = check(cudaMemcpy(buf.data(), t->T.slots, c * cell, cudaMemcpyDeviceToHost), "read cells");
+  if (rc) return rc;
+  const size_t voff = t->cfg.layout == CH_PACKED ? 4 : (cell == 16 ? 8 : 4);
+  for (uint64_t i = 0; i < c; ++i) {
+    const unsigned char* p = buf.data() + i * cell;
+    if (h_keys) memcpy((char*)h_keys + i * kb, p, kb);
+    if (h_vals) memcpy((char*)h_vals + i * vb, p + voff, vb);
+  }
+  return CH_OK;
+}
+
+int ch_write_slots(ch_table* t, const void* h_keys, const void* h_vals) {
+  if (!t || !h_keys || !h_vals) return fail(CH_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard dev(t->cfg.device);
+  int rc = check(cudaEventSynchronize(t->last), "synchronize");
+  if (rc) return rc;
+  const uint64_t c = t->T.c;
+  const int kb = t->ts.kbytes, vb = t->ts.vbytes;
+  if (t->cfg.layout == CH_SOA) {
+    rc = check(cudaMemcpy(t->T.slots, h_keys, c * kb, cudaMemcpyHostToDevice), "write keys");
+    if (!rc) rc = check(cudaMemcpy(t->T.vals, h_vals, c * vb, cudaMemcpyHostToDevice), "write values");
+    return rc;
+  }
+  const size_t cell = t->cfg.layout == CH_PACKED ? 8 : (kb == 8 || vb == 8 ? 16 : 8);
+  const size_t voff = t->cfg.layout == CH_PACKED ? 4 : (cell == 16 ? 8 : 4);
+  std::vector<unsigned char> buf(c * cell, 0);
+  for (uint64_t i = 0; i < c; ++i) {
+    memcpy(buf.data() + i * cell, (const char*)h_keys + i * kb, kb);
+    memcpy(buf.data() + i * cell + voff, (const char*)h_vals + i * vb, vb);
+  }
+  return check(cudaMemcpy(t->T.slots, buf.data(), c * cell, cudaMemcpyHostToDevice), "write cells");
+}
+
+int ch_read_arena(ch_table* t, void* h_arena, uint64_t count) {
+  if (!t || !h_arena) return fail(CH_EINVAL, "null argument");
+  if (t->cfg.kind != CH_BUCKET) return fail(CH_EINVAL, "not a bucket-list table");
+  if (count > t->cfg.pool_capacity) count = t->cfg.pool_capacity;
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard dev(t->cfg.device);
+  int rc = check(cudaEventSynchronize(t->last), "synchronize");
+  if (rc) return rc;
+  return check(cudaMemcpy(h_arena, t->arena, count * t->vbytes, cudaMemcpyDeviceToHost), "read arena");
+}
+
+int ch_slot_op(ch_table* t, int op, uint64_t slot, uint64_t expected, uint64_t desired, uint64_t value, int* h_won,
+               uint64_t* h_key, uint64_t* h_val) {
+  if (!t || !h_won || !h_key || !h_val) return fail(CH_EINVAL, "null argument");
+  if (slot >= t->T.c) return fail(CH_EINVAL, "slot out of range");
+  if (op < 0 || op > 5) return fail(CH_EINVAL, "bad slot op");
+  if (t->cfg.layout == CH_PACKED && op == 2) return fail(CH_EINVAL, "value CAS is not available on packed cells");
+  if (t->cfg.layout != CH_PACKED && op == 1) return fail(CH_EINVAL, "pair claim requires the packed layout");
+  Ordered o(t, nullptr);
+  Scratch sc(o.s);
+  unsigned long long* d = (unsigned long long*)sc.get(24);
+  if (!d) return o.done(fail(CH_ENOMEM, "scratch"));
+  const int kb = t->ts.kbytes, vb = t->ts.vbytes;
+  if (kb == 4 && vb == 4) k_slot_op<uint32_t, uint32_t><<<1, 1, 0, o.s>>>(t->T, t->cfg.layout, op, slot, expected, desired, value, d);
+  else if (kb == 4) k_slot_op<uint32_t, uint64_t><<<1, 1, 0, o.s>>>(t->T, t->cfg.layout, op, slot, expected, desired, value, d);
+  else if (vb == 4) k_slot_op<uint64_t, uint32_t><<<1, 1, 0, o.s>>>(t->T, t->cfg.layout, op, slot, expected, desired, value, d);
+  else k_slot_op<uint64_t, uint64_t><<<1, 1, 0, o.s>>>(t->T, t->cfg.layout, op, slot, expected, desired, value, d);
+  int rc = check(cudaGetLastError(), "slot op");
+  unsigned long long hbuf[3] = {0, 0, 0};
+  if (!rc) rc = check(cudaMemcpyAsync(hbuf, d, 24, cudaMemcpyDeviceToHost, o.s), "slot op read");
+  if (!rc) rc = check(cudaStreamSynchronize(o.s), "slot op sync");
+  *h_won = (int)hbuf[0];
+  *h_key = hbuf[1];
+  *h_val = hbuf[2];
+  return o.done(rc);
+}
+
+// ---- device primitives ----
+static Launch plain_launch(int device, void* stream) {
+  Launch lc;
+  lc.stream = (cudaStream_t)stream;
+  lc.device = device;
+  lc.sms = 148;
+  cudaDeviceGetAttribute(&lc.sms, cudaDevAttrMultiProcessorCount, device);
+  return lc;
+}
+
+int ch_exclusive_scan_u32(const uint32_t* counts, uint64_t n, uint64_t* out, int device, void* stream) {
+  if (!out || (n && !counts)) return fail(CH_EINVAL, "null buffer");
+  DeviceGuard dev(device);
+  Launch lc = plain_launch(device, stream);
+  Scratch sc(lc.stream);
+  const size_t sb = exclusive_scan_scratch_bytes(n);
+  void* p = sc.get(sb);
+  if (!p) return fail(CH_ENOMEM, "scratch allocation failed");
+  return exclusive_scan_u32(lc, counts, n, out, p, sb);
+}
+
+int ch_mix64(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t* out, int device, void* stream) {
+  if (n && (!keys || !out)) return fail(CH_EINVAL, "null buffer");
+  DeviceGuard dev(device);
+  return mix64_array(plain_launch(device, stream), keys, n, seed, out);
+}
+
+int ch_multi_split(const void* keys, int key_bytes, const void* vals, int val_bytes, uint64_t n, uint32_t shards,
+                   uint64_t* perm, uint64_t* offsets, void* keys_out, void* vals_out, int device, void* stream) {
+  if (!offsets || (n && (!keys || !perm))) return fail(CH_EINVAL, "null buffer");
+  if (key_bytes != 4 && key_bytes != 8) return fail(CH_EINVAL, "key_bytes must be 4 or 8");
+  if (vals && val_bytes != 4 && val_bytes != 8) return fail(CH_EINVAL, "val_bytes must be 4 or 8");
+  DeviceGuard dev(device);
+  Launch lc = plain_launch(device, stream);
+  Scratch sc(lc.stream);
+  const size_t sb = split_scratch_bytes(n, shards);
+  void* p = sc.get(sb);
+  if (!p) return fail(CH_ENOMEM, "scratch allocation failed");
+  return multi_split(lc, keys, key_bytes, vals, vals ? val_bytes : 4, n, shards, perm, offsets, keys_out, vals_out,
+                     p, sb);
+}
+
+int ch_partition(const uint32_t* dest, uint64_t n, uint32_t shards, uint64_t* perm, uint64_t* offsets, int device,
+                 void* stream) {
+  if (!offsets || (n && (!dest || !perm))) return fail(CH_EINVAL, "null buffer");
+  DeviceGuard dev(device);
+  Launch lc = plain_launch(device, stream);
+  Scratch sc(lc.stream);
+  const size_t sb = split_scratch_bytes(n, shards);
+  void* p = sc.get(sb);
+  if (!p) return fail(CH_ENOMEM, "scratch allocation failed");
+  return multi_split(lc, dest, 0, nullptr, 4, n, shards, perm, offsets, nullptr, nullptr, p, sb);
+}
+
+int ch_scatter(const void* src, int elem_bytes, const uint64_t* perm, uint64_t n, void* dst, int device,
+               void* stream) {
+  if (n && (!src || !perm || !dst)) return fail(CH_EINVAL, "null buffer");
+  DeviceGuard dev(device);
+  return permute(plain_launch(device, stream), src, elem_bytes, perm, n, dst, true);
+}
+
+int ch_gather(const void* src, int elem_bytes, const uint64_t* perm, uint64_t n, void* dst, int device,
+              void* stream) {
+  if (n && (!src || !perm || !dst)) return fail(CH_EINVAL, "null buffer");
+  DeviceGuard dev(device);
+  return permute(plain_launch(device, stream), src, elem_bytes, perm, n, dst, false);
+}
+
+int ch_segment_copy(const void* src, int elem_bytes, const uint64_t* src_off, const uint64_t* idx, uint64_t n,
+                    const uint64_t* dst_off, void* dst, int device, void* stream) {
+  if (n && (!src_off || !idx || !dst_off)) return fail(CH_EINVAL, "null buffer");
+  DeviceGuard dev(device);
+  return segment_copy(plain_launch(device, stream), src, elem_bytes, src_off, idx, n, dst_off, dst);
+}
+
+}  // extern "C"

@@ -1,0 +1,316 @@
+// bucket.cu -- bucket-list table kernels (bucket_list.py).
+//
+// The reference appends one value at a time through a CAS state machine on
+// the key's 64-bit list handle (state | count | tail, :61-70), growing the
+// chain bucket by bucket from a bump arena (:228-294).  A GPU batch instead
+// aggregates all appends of one key first, so each key's handle moves ONCE
+// per batch with no contention:
+//   1. find_or_claim every key in the key store                (single.cu K1 MODE 1)
+//   2. rank[i] = atomicAdd(batch_count[slot])                  k_bucket_rank
+//   3. per key-store slot: how many values fit, how many arena
+//      cells the new buckets need                              k_bucket_need
+//   4. exclusive scan of the needs -> contention-free bump offsets (prims.cu)
+//   5. per slot: carve its buckets, link the headers, publish the
+//      new handle (READY, or FULL once the pool/count limit hits) k_bucket_alloc
+//      (pool exhaustion falls back to the reference's bucket-by-bucket order in
+//      k_bucket_alloc_seq, so OUT_OF_MEMORY stays per key and sticky)
+//   6. every pair writes its value at the arena cell its index maps to    k_bucket_write
+// The chain geometry is a pure function of the growth policy (:11-15), so the
+// arena cell of value index v is computed, never searched.
+#include "bucket.cuh"
+#include "dispatch.cuh"
+#include "probe.cuh"
+
+namespace chb {
+
+template <typename K>
+__device__ __forceinline__ uint64_t* handle_ptr(const TableRef& T, Layout lay, uint64_t s) {
+  if (lay == SOA) return static_cast<uint64_t*>(T.vals) + s;
+  return &static_cast<CellT<K, uint64_t>*>(T.slots)[s].v;
+}
+
+__global__ void k_bucket_rank(const int64_t* __restrict__ slots, uint64_t n, uint32_t* __restrict__ bcnt,
+                              uint32_t* __restrict__ rank) {
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t s = slots[i];
+    if (s >= 0) rank[i] = atomicAdd(bcnt + s, 1u);
+  }
+}
+
+template <typename K>
+__global__ void k_bucket_need(BucketRef B, Layout lay, uint64_t* __restrict__ need_out) {
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < B.T.c; s += stride) {
+    const uint32_t m = B.bcnt[s];
+    uint64_t need = 0;
+    if (m) {
+      const uint64_t h = *handle_ptr<K>(B.T, lay, s);
+      const uint64_t state = h >> (COUNT_BITS + TAIL_BITS), count = (h >> TAIL_BITS) & COUNT_MAX,
+                     tail = h & TAIL_MAX;
+      BucketInfo in;
+      in.region = 0;
+      in.tail_old = tail;
+      in.c0 = state == H_UNINIT ? 0 : (uint32_t)count;
+      in.overflow = 0;
+      in.pad = 0;
+      if (state == H_FULL) {  // sticky (:245-246)
+        in.fit = 0;
+        in.new_count = count;
+      } else {
+        uint64_t fit = m;
+        if (in.c0 + fit > COUNT_MAX) {  // count >= COUNT_MAX -> FULL (:261-264)
+          fit = COUNT_MAX - in.c0;
+          in.overflow = 1;
+        }
+        in.fit = (uint32_t)fit;
+        in.new_count = in.c0 + fit;
+        const uint64_t have = B.gr.before(B.gr.buckets_for(in.c0));  // capacity of the current chain
+        if (in.new_count > have) {
+          const uint64_t b0 = B.gr.buckets_for(in.c0);  // first new bucket
+          const uint64_t b1 = B.gr.buckets_for(in.new_count) - 1;
+          need = B.gr.cells(b0, b1);
+        }
+      }
+      in.need = need;
+      B.info[s] = in;
+    }
+    need_out[s] = need;
+  }
+}
+
+// Carve the new buckets of slot s starting at arena offset `region`, link the
+// headers, return the tail.  b0..b1 are the new bucket indices.
+__device__ __forceinline__ uint64_t link_buckets(const BucketRef& B, uint64_t region, uint64_t b0, uint64_t b1,
+                                                 uint64_t prev_tail, int vbytes) {
+  uint64_t base = region, prev = prev_tail;
+  for (uint64_t b = b0; b <= b1; ++b) {
+    if (b > 0) {  // leading cell references the previous bucket (:288)
+      if (vbytes == 8) static_cast<uint64_t*>(B.arena)[base] = prev;
+      else static_cast<uint32_t*>(B.arena)[base] = (uint32_t)prev;
+    }
+    prev = base;
+    base += B.gr.size(b) + (b > 0 ? 1 : 0);
+  }
+  return prev;
+}
+
+template <typename K>
+__global__ void k_bucket_alloc(BucketRef B, Layout lay, const uint64_t* __restrict__ alloc_off, int vbytes) {
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  const unsigned long long bump0 = *B.bump;
+  long long values = 0;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < B.T.c; s += stride) {
+    if (!B.bcnt[s]) continue;
+    BucketInfo in = B.info[s];
+    uint64_t* hp = handle_ptr<K>(B.T, lay, s);
+    const uint64_t h = *hp;
+    if ((h >> (COUNT_BITS + TAIL_BITS)) == H_FULL) continue;
+    uint64_t tail = in.tail_old;
+    if (in.need) {
+      const uint64_t off = bump0 + alloc_off[s];
+      if (off + in.need > B.pool_cap) {  // pool exhausted from here on: sequential fallback
+        B.info[s].fit = FIT_DEFERRED;
+        atomicMin(B.first_fail, (unsigned long long)s);
+        continue;
+      }
+      const uint64_t b0 = B.gr.buckets_for(in.c0);
+      const uint64_t b1 = B.gr.buckets_for(in.new_count) - 1;
+      tail = link_buckets(B, off, b0, b1, in.tail_old, vbytes);
+      B.info[s].region = off;
+    }
+    *hp = pack_handle(in.overflow ? H_FULL : H_READY, in.new_count, tail);
+    values += in.fit;
+  }
+  const long long v[1] = {values};
+  long long* const dst[1] = {&B.T.ctr->total_values};
+  cta_add<1>(v, dst);
+}
+
+// Pool exhausted: from the first failing slot on, allocate bucket by bucket in
+// slot order exactly like the reference's sequential appends (:252-255, :283-287).
+template <typename K>
+__global__ void k_bucket_alloc_seq(BucketRef B, Layout lay, const uint64_t* __restrict__ alloc_off, int vbytes) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const unsigned long long ff = *B.first_fail;
+  const unsigned long long bump0 = *B.bump;
+  if (ff == ~0ull) {  // everything fit: advance the bump by the total
+    *B.bump = bump0 + alloc_off[B.T.c];
+    B.T.ctr->pool_used += alloc_off[B.T.c];
+    return;
+  }
+  uint64_t cursor = bump0 + alloc_off[ff];
+  long long values = 0;
+  for (uint64_t s = ff; s < B.T.c; ++s) {
+    if (!B.bcnt[s] || B.info[s].fit != FIT_DEFERRED) continue;
+    BucketInfo in = B.info[s];
+    uint64_t* hp = handle_ptr<K>(B.T, lay, s);
+    const uint64_t b0 = B.gr.buckets_for(in.c0);
+    const uint64_t b1 = B.gr.buckets_for(in.new_count) - 1;
+    uint64_t prev = in.tail_old, cap = B.gr.before(b0), region = cursor;
+    bool failed = false;
+    for (uint64_t b = b0; b <= b1; ++b) {
+      const uint64_t cells = B.gr.size(b) + (b > 0 ? 1 : 0);
+      if (cursor + cells > B.pool_cap) { failed = true; break; }
+      if (b > 0) {
+        if (vbytes == 8) static_cast<uint64_t*>(B.arena)[cursor] = prev;
+        else static_cast<uint32_t*>(B.arena)[cursor] = (uint32_t)prev;
+      }
+      prev = cursor;
+      cursor += cells;
+      cap += B.gr.size(b);
+    }
+    const uint64_t fit = failed ? (cap > in.c0 ? cap - in.c0 : 0) : in.fit;
+    const uint64_t count = in.c0 + (fit < in.fit ? fit : in.fit);
+    B.info[s].fit = (uint32_t)(fit < in.fit ? fit : in.fit);
+    B.info[s].region = region;
+    const bool full = failed || in.overflow;
+    // an UNINITIALIZED key whose first bucket does not fit becomes FULL(0, 0) (:254)
+    *hp = pack_handle(full ? H_FULL : H_READY, count, count == 0 ? 0 : prev);
+    values += B.info[s].fit;
+  }
+  B.T.ctr->pool_used += cursor - bump0;
+  B.T.ctr->total_values += values;
+  *B.bump = cursor;
+}
+
+template <typename V>
+__global__ void k_bucket_write(BucketRef B, const int64_t* __restrict__ slots, const uint32_t* __restrict__ rank,
+                               const V* __restrict__ vals, uint64_t n, uint8_t* __restrict__ status) {
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  V* arena = static_cast<V*>(B.arena);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t s = slots[i];
+    if (s < 0) continue;  // INVALID_KEY / TABLE_FULL from the key store stay
+    const BucketInfo in = B.info[s];
+    const uint32_t r = rank[i];
+    if (r >= in.fit) {
+      status[i] = ST_OOM;
+      continue;
+    }
+    const uint64_t v = (uint64_t)in.c0 + r;  // value index in the key's chain
+    const uint64_t b = B.gr.buckets_for(v + 1) - 1;
+    const uint64_t within = v - B.gr.before(b);
+    uint64_t base;
+    const uint64_t b_new0 = B.gr.buckets_for(in.c0);
+    if (in.c0 > 0 && b + 1 == b_new0) {
+      base = in.tail_old;  // room left in the old tail bucket (:266-276)
+    } else {
+      base = in.region + (B.gr.before(b) - B.gr.before(b_new0)) + (b - b_new0) -
+             ((b_new0 == 0 && b > 0) ? 1 : 0);
+    }
+    arena[base + (b > 0 ? 1 : 0) + within] = ld_stream(vals + i);
+    status[i] = ST_INSERTED;
+  }
+}
+
+__global__ void k_bucket_reset(const int64_t* __restrict__ slots, const uint32_t* __restrict__ rank, uint64_t n,
+                               uint32_t* __restrict__ bcnt) {
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t s = slots[i];
+    if (s >= 0 && rank[i] == 0) bcnt[s] = 0;
+  }
+}
+
+// counts from handles (:320-326): the lookup wrote handle 0 for absent keys
+__global__ void k_handle_counts(const uint64_t* __restrict__ handles, uint64_t n, uint32_t* __restrict__ counts) {
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    counts[i] = (uint32_t)((handles[i] >> TAIL_BITS) & COUNT_MAX);
+}
+
+// chain walk, tail -> head through the prev links, values emitted head first (:328-355)
+template <typename V>
+__global__ void k_bucket_walk(BucketRef B, const uint64_t* __restrict__ handles, uint64_t n,
+                              const uint64_t* __restrict__ offsets, V* __restrict__ out) {
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  const V* arena = static_cast<const V*>(B.arena);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t want = offsets[i + 1] - offsets[i];
+    if (!want) continue;
+    const uint64_t h = handles[i];
+    const uint64_t count = (h >> TAIL_BITS) & COUNT_MAX;
+    const uint64_t take_all = count < want ? count : want;  // raced writer: keep the segment length
+    uint64_t base = h & TAIL_MAX;
+    const uint64_t m = B.gr.buckets_for(count);
+    for (uint64_t bb = m; bb-- > 0;) {
+      const uint64_t first = B.gr.before(bb);
+      if (first < take_all) {
+        const uint64_t sz = B.gr.size(bb);
+        const uint64_t take = (take_all - first) < sz ? (take_all - first) : sz;
+        const uint64_t src = base + (bb > 0 ? 1 : 0);
+        for (uint64_t k = 0; k < take; ++k) out[offsets[i] + first + k] = arena[src + k];
+      }
+      if (bb > 0) base = (uint64_t)arena[base];
+    }
+  }
+}
+
+// ------------------------------------------------------------ host side
+int bucket_insert(const Launch& lc, const BucketRef& B, const TypeSel& ts, const void* keys, const void* vals,
+                  uint64_t n, uint8_t* status, int64_t* slots, uint32_t* rank, uint64_t* need, uint64_t* alloc_off,
+                  void* scan_scratch, size_t scan_bytes) {
+  const Layout lay = (Layout)ts.layout;
+  TypeSel kts = ts;
+  kts.vbytes = 8;  // key store values are 64-bit handles
+  int rc = single_insert(lc, B.T, kts, keys, nullptr, n, status, slots, 1);
+  if (rc) return rc;
+  rc = launch_persistent(lc, (const void*)k_bucket_rank, n, 1, [&](dim3 g, dim3 b) {
+    k_bucket_rank<<<g, b, 0, lc.stream>>>(slots, n, B.bcnt, rank);
+  });
+  if (rc) return rc;
+  const bool k4 = ts.kbytes == 4;
+  auto need_k = k4 ? (const void*)k_bucket_need<uint32_t> : (const void*)k_bucket_need<uint64_t>;
+  rc = launch_persistent(lc, need_k, B.T.c, 1, [&](dim3 g, dim3 b) {
+    if (k4) k_bucket_need<uint32_t><<<g, b, 0, lc.stream>>>(B, lay, need);
+    else k_bucket_need<uint64_t><<<g, b, 0, lc.stream>>>(B, lay, need);
+  });
+  if (rc) return rc;
+  rc = exclusive_scan_u64(lc, need, B.T.c, alloc_off, scan_scratch, scan_bytes);
+  if (rc) return rc;
+  rc = cuda_check(cudaMemsetAsync(B.first_fail, 0xff, sizeof(unsigned long long), lc.stream), "memset");
+  if (rc) return rc;
+  auto alloc_k = k4 ? (const void*)k_bucket_alloc<uint32_t> : (const void*)k_bucket_alloc<uint64_t>;
+  rc = launch_persistent(lc, alloc_k, B.T.c, 1, [&](dim3 g, dim3 b) {
+    if (k4) k_bucket_alloc<uint32_t><<<g, b, 0, lc.stream>>>(B, lay, alloc_off, ts.vbytes);
+    else k_bucket_alloc<uint64_t><<<g, b, 0, lc.stream>>>(B, lay, alloc_off, ts.vbytes);
+  });
+  if (rc) return rc;
+  if (k4) k_bucket_alloc_seq<uint32_t><<<1, 32, 0, lc.stream>>>(B, lay, alloc_off, ts.vbytes);
+  else k_bucket_alloc_seq<uint64_t><<<1, 32, 0, lc.stream>>>(B, lay, alloc_off, ts.vbytes);
+  rc = cuda_check(cudaGetLastError(), "bucket alloc seq");
+  if (rc) return rc;
+  if (ts.vbytes == 8) {
+    rc = launch_persistent(lc, (const void*)k_bucket_write<uint64_t>, n, 1, [&](dim3 g, dim3 b) {
+      k_bucket_write<uint64_t><<<g, b, 0, lc.stream>>>(B, slots, rank, (const uint64_t*)vals, n, status);
+    });
+  } else {
+    rc = launch_persistent(lc, (const void*)k_bucket_write<uint32_t>, n, 1, [&](dim3 g, dim3 b) {
+      k_bucket_write<uint32_t><<<g, b, 0, lc.stream>>>(B, slots, rank, (const uint32_t*)vals, n, status);
+    });
+  }
+  if (rc) return rc;
+  return launch_persistent(lc, (const void*)k_bucket_reset, n, 1, [&](dim3 g, dim3 b) {
+    k_bucket_reset<<<g, b, 0, lc.stream>>>(slots, rank, n, B.bcnt);
+  });
+}
+
+int bucket_counts(const Launch& lc, const uint64_t* handles, uint64_t n, uint32_t* counts) {
+  return launch_persistent(lc, (const void*)k_handle_counts, n, 1, [&](dim3 g, dim3 b) {
+    k_handle_counts<<<g, b, 0, lc.stream>>>(handles, n, counts);
+  });
+}
+
+int bucket_walk(const Launch& lc, const BucketRef& B, int vbytes, const uint64_t* handles, uint64_t n,
+                const uint64_t* offsets, void* out) {
+  if (vbytes == 8)
+    return launch_persistent(lc, (const void*)k_bucket_walk<uint64_t>, n, 1, [&](dim3 g, dim3 b) {
+      k_bucket_walk<uint64_t><<<g, b, 0, lc.stream>>>(B, handles, n, offsets, (uint64_t*)out);
+    });
+  return launch_persistent(lc, (const void*)k_bucket_walk<uint32_t>, n, 1, [&](dim3 g, dim3 b) {
+    k_bucket_walk<uint32_t><<<g, b, 0, lc.stream>>>(B, handles, n, offsets, (uint32_t*)out);
+  });
+}
+
+}  // namespace chb

@@ -1,0 +1,271 @@
+"""Single-value hash table on B200 (mirrors coophash.single_table).
+
+Every operation is a CUDA kernel (csrc/single.cu) reached through the C ABI:
+  insert / insert_bulk          K1 ch_insert        (single_table.py:273-290, 355-374)
+  find_or_claim                 K1 ch_find_or_claim (:292-311)
+  retrieve / retrieve_bulk      K2 ch_retrieve      (:313-327, 376-408)
+  retrieve_with_stats / slot_of ch_find             (:317-336)
+  erase                         K3 ch_erase         (:338-351)
+  for_each / for_all            ch_find / slot read-back (:412-429)
+Gauges (occupied, tombstones, probe counters) are device counters reduced per
+CTA and read back on demand (ch_get_stats).
+
+The list API keeps the reference's signatures and return types.  The
+``*_device`` methods take and return CUDA tensors (no host round trip).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+from typing import Callable, Iterable, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _io, _lib
+from .layout import DeviceTable, LayoutKind, Sentinels, SlotArray, as_layout, default_sentinels
+from .probing import CapacityPlan, ProbingConfig, ProbingScheme, choose_capacity
+
+
+class InsertStatus(Enum):
+    INSERTED = "inserted"
+    DUPLICATE_KEY = "duplicate_key"
+    TABLE_FULL = "table_full"
+    INVALID_KEY = "invalid_key"
+    OUT_OF_MEMORY = "out_of_memory"
+
+
+STATUS_BY_CODE = tuple(InsertStatus)
+
+
+@dataclass(frozen=True)
+class ProbeStats:
+    attempts: int
+    windows_visited: int
+
+
+@dataclass
+class ProbeCounters:
+    ops: int = 0
+    attempts: int = 0
+    windows_visited: int = 0
+
+    @property
+    def mean_attempts(self) -> float:
+        return self.attempts / self.ops if self.ops else 0.0
+
+
+def statuses_from_codes(codes: np.ndarray) -> list[InsertStatus]:
+    return [STATUS_BY_CODE[c] for c in codes.tolist()]
+
+
+class _TableBase:
+    """Construction and gauges shared by the three table kinds."""
+
+    _kind = _lib.CH_SINGLE
+
+    def _setup(self, min_capacity, *, layout, key_bits, value_bits, sentinels, group_width,
+               scheme, max_outer_attempts, workers, plan, device, pool_capacity=0,
+               growth=(0, 0, 0), handle_bits=None):
+        layout = as_layout(layout)
+        if plan is None:
+            plan = choose_capacity(max(min_capacity, 32))
+        self.config = ProbingConfig(plan=plan, scheme=scheme, group_width=group_width,
+                                    max_outer_attempts=max_outer_attempts)
+        if sentinels is None:
+            sentinels = default_sentinels(key_bits)
+        vbits = handle_bits if handle_bits is not None else value_bits
+        if layout == LayoutKind.PACKED_AOS and (key_bits > 32 or vbits > 32):
+            from .layout import LayoutUnsupported
+            raise LayoutUnsupported("packed layout needs 32-bit keys and values")
+        self._dt = DeviceTable(kind=self._kind, layout=layout, key_bits=key_bits, value_bits=value_bits,
+                               group_width=group_width, p=plan.p,
+                               max_outer_attempts=self.config.max_outer_attempts,
+                               sentinels=sentinels, device=device, pool_capacity=pool_capacity,
+                               growth=growth)
+        self.key_bits, self.value_bits = key_bits, value_bits
+        self.layout = layout
+        self.workers = workers
+        self.device = self._dt.device
+        self._packed = layout == LayoutKind.PACKED_AOS
+        self.slots = SlotArray(plan.c, layout, sentinels, key_bits=key_bits, value_bits=vbits,
+                               _table=self._dt)
+        self.sentinels = sentinels
+
+    # -- introspection ---------------------------------------------------
+    @property
+    def capacity(self) -> int:
+        return self._dt.capacity
+
+    @property
+    def occupied(self) -> int:
+        return int(self._dt.stats().occupied)
+
+    def load_factor(self) -> float:
+        return self.occupied / self.capacity
+
+    def probe_counters(self) -> ProbeCounters:
+        s = self._dt.stats()
+        return ProbeCounters(ops=int(s.ops), attempts=int(s.attempts), windows_visited=int(s.windows))
+
+    def reset_probe_counters(self) -> None:
+        _lib.check(_lib.lib().ch_reset_probe_counters(self._dt.handle, self._stream()),
+                   "reset_probe_counters")
+
+    def synchronize(self) -> None:
+        _lib.check(_lib.lib().ch_synchronize(self._dt.handle), "synchronize")
+
+    # -- helpers -----------------------------------------------------------
+    def _stream(self, stream=None) -> int:
+        return _io.stream_of(self.device, stream)
+
+    def _keys(self, keys) -> torch.Tensor:
+        return _io.to_device(keys, self.key_bits, self.device, "key")
+
+    def _vals(self, vals) -> torch.Tensor:
+        return _io.to_device(vals, self.value_bits, self.device, "value")
+
+    def _empty_vals(self, n: int) -> torch.Tensor:
+        return torch.empty(n, dtype=_io.torch_dtype(self.value_bits), device=f"cuda:{self.device}")
+
+    def _u8(self, n: int) -> torch.Tensor:
+        return torch.empty(n, dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    def _is_sentinel(self, key: int) -> bool:
+        return self.sentinels.is_sentinel(key)
+
+
+class SingleValueHashTable(_TableBase):
+    """Concurrent open-addressing table mapping each key to one value (HBM-resident)."""
+
+    _kind = _lib.CH_SINGLE
+
+    def __init__(self, min_capacity: int, *, layout: LayoutKind | str = LayoutKind.SOA,
+                 key_bits: int = 64, value_bits: int = 64, sentinels: Sentinels | None = None,
+                 group_width: int = 32, scheme: ProbingScheme = ProbingScheme.COOPERATIVE,
+                 max_outer_attempts: int | None = None, workers: int = 1,
+                 plan: CapacityPlan | None = None, device=None):
+        self._setup(min_capacity, layout=layout, key_bits=key_bits, value_bits=value_bits,
+                    sentinels=sentinels, group_width=group_width, scheme=scheme,
+                    max_outer_attempts=max_outer_attempts, workers=workers, plan=plan, device=device)
+
+    @property
+    def tombstones(self) -> int:
+        return int(self._dt.stats().tombstones)
+
+    # -- device-native bulk API -----------------------------------------------
+    def insert_device(self, keys, values, status: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """K1 over CUDA tensors; returns the uint8 InsertStatus codes."""
+        k, v = self._keys(keys), self._vals(values)
+        if k.numel() != v.numel():
+            raise ValueError("keys and values differ in length")
+        n = k.numel()
+        st = status if status is not None else self._u8(n)
+        _lib.check(_lib.lib().ch_insert(self._dt.handle, k.data_ptr(), v.data_ptr(), n, st.data_ptr(),
+                                        self._stream(stream)), "insert")
+        self._dt.touch()
+        return st
+
+    def retrieve_device(self, keys, values_out: torch.Tensor | None = None,
+                        found_out: torch.Tensor | None = None, stream=None):
+        """K2 over CUDA tensors; returns (values, found) (values of misses are 0)."""
+        k = self._keys(keys)
+        n = k.numel()
+        vals = values_out if values_out is not None else self._empty_vals(n)
+        found = found_out if found_out is not None else self._u8(n)
+        _lib.check(_lib.lib().ch_retrieve(self._dt.handle, k.data_ptr(), n, vals.data_ptr(),
+                                          found.data_ptr(), self._stream(stream)), "retrieve")
+        return vals, found
+
+    def erase_device(self, keys, stream=None) -> torch.Tensor:
+        k = self._keys(keys)
+        n = k.numel()
+        out = self._u8(n)
+        _lib.check(_lib.lib().ch_erase(self._dt.handle, k.data_ptr(), n, out.data_ptr(),
+                                       self._stream(stream)), "erase")
+        self._dt.touch()
+        return out
+
+    def find_device(self, keys, *, with_stats: bool = False, with_values: bool = False, stream=None):
+        k = self._keys(keys)
+        n = k.numel()
+        dev = f"cuda:{self.device}"
+        slots = torch.empty(n, dtype=torch.int64, device=dev)
+        att = torch.empty(n, dtype=torch.int32, device=dev) if with_stats else None
+        win = torch.empty(n, dtype=torch.int32, device=dev) if with_stats else None
+        vals = self._empty_vals(n) if with_values else None
+        _lib.check(_lib.lib().ch_find(self._dt.handle, k.data_ptr(), n, slots.data_ptr(),
+                                      att.data_ptr() if att is not None else None,
+                                      win.data_ptr() if win is not None else None,
+                                      vals.data_ptr() if vals is not None else None,
+                                      self._stream(stream)), "find")
+        return slots, att, win, vals
+
+    # -- element operations (single_table.py:273-351) ---------------------------
+    def insert(self, key: int, value: int) -> InsertStatus:
+        return self.insert_bulk([(key, value)])[0]
+
+    def find_or_claim(self, key: int) -> tuple[InsertStatus, int]:
+        k = self._keys([key])
+        st = self._u8(1)
+        slots = torch.empty(1, dtype=torch.int64, device=f"cuda:{self.device}")
+        _lib.check(_lib.lib().ch_find_or_claim(self._dt.handle, k.data_ptr(), 1, st.data_ptr(),
+                                               slots.data_ptr(), self._stream()), "find_or_claim")
+        self._dt.touch()
+        return STATUS_BY_CODE[int(st.item())], int(slots.item())
+
+    def retrieve(self, key: int) -> Optional[int]:
+        return self.retrieve_bulk([key])[0]
+
+    def retrieve_with_stats(self, key: int) -> tuple[Optional[int], ProbeStats]:
+        if self._is_sentinel(key):
+            return None, ProbeStats(0, 0)
+        slots, att, win, vals = self.find_device([key], with_stats=True, with_values=True)
+        slot = int(slots.item())
+        stats = ProbeStats(int(att.item()), int(win.item()))
+        if slot < 0:
+            return None, stats
+        return int(_io.from_device(vals, self.value_bits)[0]), stats
+
+    def slot_of(self, key: int) -> int:
+        if self._is_sentinel(key):
+            return -1
+        return int(self.find_device([key])[0].item())
+
+    def erase(self, key: int) -> bool:
+        if self._is_sentinel(key):
+            return False
+        return bool(self.erase_device([key]).item())
+
+    # -- bulk operations (single_table.py:355-408) ------------------------------
+    def insert_bulk(self, pairs: Sequence[tuple[int, int]], workers: int | None = None) -> list[InsertStatus]:
+        keys, vals = _io.split_pairs(pairs)
+        if not keys:
+            return []
+        st = self.insert_device(keys, vals)
+        return statuses_from_codes(st.cpu().numpy())
+
+    def retrieve_bulk(self, keys: Sequence[int], workers: int | None = None) -> list[Optional[int]]:
+        keys = list(keys)
+        if not keys:
+            return []
+        vals, found = self.retrieve_device(keys)
+        v = _io.from_device(vals, self.value_bits).tolist()
+        f = found.cpu().numpy().tolist()
+        return [x if hit else None for x, hit in zip(v, f)]
+
+    # -- callbacks (single_table.py:412-429) ------------------------------------
+    def for_each(self, keys: Iterable[int], callback: Callable[[int, int, int], None]) -> None:
+        keys = [k for k in keys if not self._is_sentinel(k)]
+        if not keys:
+            return
+        slots, _, _, vals = self.find_device(keys, with_values=True)
+        s = slots.cpu().numpy().tolist()
+        v = _io.from_device(vals, self.value_bits).tolist()
+        for k, slot, val in zip(keys, s, v):
+            if slot >= 0:
+                callback(k, val, slot)
+
+    def for_all(self, callback: Callable[[int, int, int], None]) -> None:
+        for i, k, v in self.slots.iter_items():
+            callback(k, v, i)
