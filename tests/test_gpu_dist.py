@@ -1,0 +1,148 @@
+"""GPU parity: distribution layer (K10 split, K11 scatter, DistributedTable)."""
+import os
+import random
+from collections import Counter
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from gold import ints, load
+
+pytestmark = pytest.mark.gpu
+
+from paper_2009_07914_b200 import (DistributedTable, InsertStatus, MultiValueHashTable,  # noqa: E402
+                                   ShardMode, ShardRouter, SingleValueHashTable, multi_split)
+from paper_2009_07914_b200.distributed import ShardedTable, split_device  # noqa: E402
+
+INSERTED = InsertStatus.INSERTED
+
+
+def test_split_matches_golden_plans():
+    g = load("distributed.json")
+    keys = ints(g["keys"])
+    for s, plan in g["splits"].items():
+        p = multi_split(keys, ShardRouter(int(s)))
+        assert p.permutation == plan["perm"] and p.offsets == plan["offsets"]
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3, 8, 37, 256])
+def test_large_split_is_stable_and_exact(shards):
+    n = (1 << 20) + 123
+    rng = np.random.default_rng(shards)
+    keys = rng.integers(0, 1 << 63, size=n, dtype=np.uint64)
+    vals = rng.integers(0, 1 << 31, size=n, dtype=np.uint64).astype(np.uint32)
+    k = torch.from_numpy(keys.view(np.int64)).cuda()
+    v = torch.from_numpy(vals.view(np.int32)).cuda()
+    perm, offsets, kout, vout = split_device(k, shards, v)
+    rperm, roff = orc.multi_split(keys, shards)
+    assert (perm.cpu().numpy() == rperm.astype(np.int64)).all()
+    assert (offsets.cpu().numpy() == roff.astype(np.int64)).all()
+    assert (kout.cpu().numpy().view(np.uint64) == keys[rperm]).all()
+    assert (vout.cpu().numpy().view(np.uint32) == vals[rperm]).all()
+
+
+def test_custom_router_partition():          # test_distributed.py:15-23,36-48
+    class Fixed:
+        def __init__(self, mapping, num_shards):
+            self.mapping, self.num_shards = mapping, num_shards
+
+        def route(self, key):
+            return self.mapping[key]
+
+    keys = ["a", "b", "c", "d"]
+    plan = multi_split(keys, Fixed({"a": 1, "b": 0, "c": 1, "d": 0}, 2))
+    assert [keys[i] for i in plan.permutation] == ["b", "d", "a", "c"]
+    assert plan.offsets == [0, 2, 4] and plan.segment(0) == [1, 3]
+    assert multi_split([10, 20, 30], ShardRouter(1)).permutation == [0, 1, 2]
+
+
+def _workload(n=4096, r=8, seed=9):
+    rng = random.Random(seed)
+    return [(rng.randrange(1, n // r + 1), i) for i, _ in enumerate(range(n), start=1)]
+
+
+def test_distributed_multi_equals_monolithic():   # test_distributed.py:82-96
+    pairs = _workload()
+    n = len(pairs)
+    mono = MultiValueHashTable(int(n / 0.8))
+    mono.insert_bulk(pairs)
+    with DistributedTable(4, lambda s: MultiValueHashTable(int(n / 4 / 0.7))) as dt:
+        assert all(st == INSERTED for st in dt.insert_bulk(pairs))
+        queries = sorted({k for k, _ in pairs}) + [99_999]
+        offsets, flat = dt.retrieve_bulk(queries)
+        mo, mf = mono.retrieve_bulk(queries)
+        for i in range(len(queries)):
+            assert sorted(flat[offsets[i]:offsets[i + 1]]) == sorted(mf[mo[i]:mo[i + 1]])
+        for k in {k for k, _ in pairs}:
+            holders = [s for s, t in enumerate(dt.shards) if t.count(k) > 0]
+            assert holders == [dt.router.route(k)]
+        assert dt.count_bulk(queries) == mono.count_bulk(queries)
+
+
+def test_distributed_single_vs_golden():
+    g = load("distributed.json")
+    pairs = [tuple(p) for p in g["pairs"]]
+    dup_keys = {k for k, c in Counter(k for k, _ in pairs).items() if c > 1}
+    for s_str, exp in g["single"].items():
+        S = int(s_str)
+        with DistributedTable(S, lambda _: SingleValueHashTable(4096)) as dt:
+            st = dt.insert_bulk(pairs)
+            for (k, _), got, ref in zip(pairs, st, exp["status"]):
+                if k not in dup_keys:
+                    assert got.value == ref
+            got = dt.retrieve_bulk(list(range(0, 3005)))
+            for k, a, b in zip(range(3005), got, exp["retrieve"]):
+                if k in dup_keys:
+                    assert (a is None) == (b is None)
+                    assert a in {v for kk, v in pairs if kk == k}
+                else:
+                    assert a == b
+
+
+def test_independent_modes():                # test_distributed.py:108-171
+    pairs = _workload(n=2048, r=4)
+    with DistributedTable(4, lambda s: MultiValueHashTable(1024), mode=ShardMode.INDEPENDENT) as dt:
+        assert all(st == INSERTED for st in dt.insert_bulk(pairs))
+        ref = Counter(k for k, _ in pairs)
+        q = sorted(ref)
+        assert dt.count_bulk(q) == [ref[x] for x in q]
+    with DistributedTable(3, lambda s: SingleValueHashTable(64), mode=ShardMode.INDEPENDENT) as dt:
+        for s, table in enumerate(dt.shards):
+            table.insert(42, 100 + s)
+        assert dt.retrieve_bulk([42]) == [100]
+    with DistributedTable(4, lambda s: MultiValueHashTable(64), mode=ShardMode.INDEPENDENT) as dt:
+        dt.insert_bulk([(k, k) for k in range(1, 41)])
+        assert [t.occupied for t in dt.shards] == [10, 10, 10, 10]
+
+
+def test_mode_equivalence_to_monolithic():   # test_distributed.py:149-162
+    pairs = _workload(n=2048, r=8, seed=13)
+    queries = sorted({k for k, _ in pairs})
+    mono = MultiValueHashTable(4096)
+    mono.insert_bulk(pairs)
+    mo, mf = mono.retrieve_bulk(queries)
+    for mode in (ShardMode.DISTRIBUTED, ShardMode.INDEPENDENT):
+        with DistributedTable(4, lambda s: MultiValueHashTable(1024), mode=mode) as dt:
+            dt.insert_bulk(pairs)
+            o, f = dt.retrieve_bulk(queries)
+            for i in range(len(queries)):
+                assert sorted(f[o[i]:o[i + 1]]) == sorted(mf[mo[i]:mo[i + 1]]), mode
+
+
+def test_sharded_table_single_rank_nccl():
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        local = SingleValueHashTable(1 << 16, layout="packed", key_bits=32, value_bits=32)
+        st = ShardedTable(local)
+        keys = torch.arange(1, 40_001, dtype=torch.int32, device="cuda")
+        assert (st.insert_device(keys, keys * 3).cpu() == 0).all()
+        v, f = st.retrieve_device(keys)
+        assert f.cpu().bool().all() and (v.cpu() == keys.cpu() * 3).all()
+    finally:
+        dist.destroy_process_group()

@@ -1,0 +1,153 @@
+"""GPU parity: multi-value tables (K4-K6) against the reference goldens and the oracle."""
+import random
+from collections import Counter
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from gold import ints, load
+
+pytestmark = pytest.mark.gpu
+
+from paper_2009_07914_b200 import (InsertStatus, MultiValueHashTable,  # noqa: E402
+                                   SingleValueHashTable, exclusive_prefix_sum)
+
+INSERTED = InsertStatus.INSERTED
+
+
+def table_from(sc):
+    return MultiValueHashTable(sc["min_capacity"], layout=sc["layout"], key_bits=sc["key_bits"],
+                               value_bits=32 if sc["layout"] == "packed" else 64, group_width=sc["group_width"])
+
+
+@pytest.mark.parametrize("idx", range(5))
+def test_sequential_replay_is_slot_exact(idx):
+    sc = load("multi.json")["scenarios"][idx]
+    t = table_from(sc)
+    keys, vals = ints(sc["keys"]), ints(sc["vals"])
+    assert [t.insert(k, v).value for k, v in zip(keys, vals)] == sc["status"]
+    q = ints(sc["queries"])
+    assert t.count_bulk(q) == sc["counts"]
+    offsets, flat = t.retrieve_bulk(q)
+    assert offsets == sc["offsets"]
+    assert flat == ints(sc["flat"])  # probe order, exactly
+    assert [t.slots.load_key(i) for i in range(t.capacity)] == ints(sc["final_keys"])
+    assert [t.slots.load_value(i) for i in range(t.capacity)] == ints(sc["final_vals"])
+    c = t.probe_counters()
+    assert (t.occupied, c.ops, c.attempts, c.windows_visited) == \
+        (sc["occupied"], sc["counters"]["ops"], sc["counters"]["attempts"], sc["counters"]["windows"])
+
+
+@pytest.mark.parametrize("idx", range(5))
+def test_bulk_replay_multiset_parity(idx):
+    sc = load("multi.json")["scenarios"][idx]
+    t = table_from(sc)
+    keys, vals = ints(sc["keys"]), ints(sc["vals"])
+    assert all(s == INSERTED for s in t.insert_bulk(list(zip(keys, vals))))
+    q = ints(sc["queries"])
+    assert t.count_bulk(q) == sc["counts"]            # counts exact
+    offsets, flat = t.retrieve_bulk(q)
+    assert offsets == sc["offsets"]                   # offsets exact
+    ref = ints(sc["flat"])
+    for i in range(len(q)):                           # values: sorted multisets per key
+        assert sorted(flat[offsets[i]:offsets[i + 1]]) == sorted(ref[offsets[i]:offsets[i + 1]])
+
+
+@pytest.mark.parametrize("r,g,layout", [(1, 8, "packed"), (16, 4, "soa"), (16, 8, "packed"),
+                                        (256, 32, "aos"), (4096, 16, "soa")])
+def test_large_multiset_vs_oracle(r, g, layout):
+    n = 1 << 17
+    rng = np.random.default_rng(r * 31 + g)
+    keys = rng.integers(1, n // r + 1, size=n, dtype=np.uint64) if r > 1 else \
+        rng.permutation(np.arange(1, n + 1, dtype=np.uint64))
+    vals = np.arange(1, n + 1, dtype=np.uint64)
+    kb = 32
+    vb = 32 if layout == "packed" else 64
+    t = MultiValueHashTable(int(np.ceil(n / 0.8)), layout=layout, key_bits=kb, value_bits=vb, group_width=g)
+    st = t.insert_device(keys, vals).cpu().numpy()
+    assert (st == 0).all()
+    q = np.arange(1, n + 1, dtype=np.uint64)
+    offsets, flat = t.retrieve_device(q)
+    offsets = offsets.cpu().numpy()
+    flat = flat.cpu().numpy().view(np.uint32 if vb == 32 else np.uint64).astype(np.uint64)
+    ref = orc.OracleMulti(int(np.ceil(n / 0.8)), group_width=g, key_bits=kb, packed=layout == "packed")
+    ref.insert_bulk(keys, vals)
+    roff, rflat = ref.retrieve_bulk(q)
+    assert (offsets == roff).all() and offsets[-1] == n
+    # per-key sorted multisets: sort within segments via (segment id, value)
+    seg = np.repeat(np.arange(n), np.diff(offsets))
+    a = np.lexsort((flat, seg))
+    b = np.lexsort((rflat, seg))
+    assert (flat[a] == rflat[b]).all()
+
+
+def test_prefix_sum_device_and_host():       # test_multi_table.py:55-66
+    assert exclusive_prefix_sum([]) == [0]
+    assert exclusive_prefix_sum([2, 0, 3]) == [0, 2, 2, 5]
+    rng = np.random.default_rng(79)
+    for n in (1, 4095, 4096, 4097, 1 << 20, (1 << 24) + 17):
+        counts = rng.integers(0, 10, size=n, dtype=np.int32)
+        dev = exclusive_prefix_sum(torch.from_numpy(counts).cuda()).cpu().numpy()
+        ref = np.concatenate([[0], np.cumsum(counts, dtype=np.int64)])
+        assert (dev == ref).all(), n
+
+
+def test_reference_semantics():              # test_multi_table.py:19-52,90-96,165-178
+    t = MultiValueHashTable(1000)
+    assert t.insert(8, 1) == INSERTED and t.insert(8, 2) == INSERTED
+    assert t.count(8) == 2 and sorted(t.retrieve(8)) == [1, 2]
+    for _ in range(10):
+        assert t.insert(3, 3) == INSERTED
+    assert t.count(3) == 10
+    t2 = MultiValueHashTable(1000)
+    t2.insert(1, 10)
+    assert t2.retrieve_bulk([999, 1, 998]) == ([0, 0, 1, 1], [10])
+    assert t2.retrieve_bulk([]) == ([0], [])
+    full = MultiValueHashTable(32)
+    for i in range(64):
+        assert full.insert(1, i) == INSERTED
+    assert full.insert(1, 64) == InsertStatus.TABLE_FULL and full.insert(2, 0) == InsertStatus.TABLE_FULL
+    e = t.slots.sentinels.empty_key
+    assert t.insert(e, 0) == InsertStatus.INVALID_KEY and t.count(e) == 0 and t.retrieve(e) == []
+
+
+def test_distinct_keys_match_single_value():  # test_multi_table.py:29-39
+    rng = random.Random(71)
+    keys = rng.sample(range(1, 1 << 30), 2000)
+    multi, single = MultiValueHashTable(4000), SingleValueHashTable(4000)
+    for k in keys:
+        assert multi.insert(k, k) == single.insert(k, k) == INSERTED
+    assert ({k: v for _, k, v in multi.slots.iter_items()} == {k: v for _, k, v in single.slots.iter_items()})
+
+
+def test_same_key_storm_all_land():          # test_multi_table.py:145-162
+    t = MultiValueHashTable(1 << 14, key_bits=32, value_bits=32, layout="packed")
+    n = 10_000
+    st = t.insert_device(torch.full((n,), 55, dtype=torch.int32, device="cuda"),
+                         torch.arange(n, dtype=torch.int32, device="cuda")).cpu().numpy()
+    assert (st == 0).all()
+    assert t.count(55) == n and sorted(t.retrieve(55)) == list(range(n))
+
+
+def test_high_multiplicity_completes():      # test_multi_table.py:113-122
+    n, r = 1 << 14, 4096
+    rng = random.Random(91)
+    keys = [rng.randrange(1, n // r + 1) for _ in range(n)]
+    t = MultiValueHashTable(int(n / 0.8))
+    assert all(s == INSERTED for s in t.insert_bulk(list(zip(keys, range(n)))))
+    assert sum(t.count(k) for k in range(1, n // r + 1)) == n
+    assert Counter(keys) == Counter({k: t.count(k) for k in range(1, n // r + 1)})
+
+
+def test_for_each_matches_retrieve_bulk():  # test_multi_table.py:99-110
+    t = MultiValueHashTable(2000)
+    rng = random.Random(89)
+    t.insert_bulk([(rng.randrange(1, 40), i) for i in range(500)])
+    queries = list(range(1, 50))
+    calls = []
+    t.for_each(queries, lambda k, v, i: calls.append((k, v)))
+    offsets, flat = t.retrieve_bulk(queries)
+    via = [(q, v) for i, q in enumerate(queries) for v in flat[offsets[i]:offsets[i + 1]]]
+    assert Counter(calls) == Counter(via)

@@ -1,0 +1,367 @@
+"""GPU parity: single-value tables (K0-K3) against the reference goldens and the oracle.
+
+Sequential (element-at-a-time) replays must reproduce the reference's slot
+placement, statuses, probe statistics and counters exactly; bulk batches run
+concurrently on the GPU and are checked for the reference's semantics
+(SURVEY.md §8c): exact statuses for distinct keys, one INSERTED per new key,
+bit-exact values and found flags.
+"""
+import zlib
+from collections import Counter
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from gold import STATUS_NAMES, ints, load
+
+pytestmark = pytest.mark.gpu
+
+from paper_2009_07914_b200 import (InsertStatus, LayoutKind, SingleValueHashTable,  # noqa: E402
+                                   probing)
+
+INSERTED, DUP = InsertStatus.INSERTED, InsertStatus.DUPLICATE_KEY
+
+
+def table_from(sc):
+    e, t = int(sc["empty"]), int(sc["tomb"])
+    from paper_2009_07914_b200 import Sentinels
+    return SingleValueHashTable(sc["min_capacity"], layout=sc["layout"], key_bits=sc["key_bits"],
+                                value_bits=32 if sc["layout"] == "packed" else 64,
+                                group_width=sc["group_width"], max_outer_attempts=sc["max_outer_attempts"],
+                                sentinels=Sentinels(e, t))
+
+
+# ------------------------------------------------ sequential replay: slot-exact
+
+@pytest.mark.parametrize("idx", range(11))
+def test_sequential_replay_is_slot_exact(idx):
+    sc = load("single.json")["scenarios"][idx]
+    t = table_from(sc)
+    assert t.capacity == sc["capacity"]
+    for step in sc["steps"]:
+        if step["op"] == "insert_bulk":
+            got = [t.insert(k, v).value for k, v in zip(ints(step["keys"]), ints(step["vals"]))]
+            assert got == step["status"]
+        elif step["op"] == "erase":
+            assert [t.erase(k) for k in ints(step["keys"])] == step["result"]
+        elif step["op"] == "retrieve_bulk":
+            got = t.retrieve_bulk(ints(step["keys"]))
+            assert got == [None if r is None else int(r) for r in step["result"]]
+        elif step["op"] == "stats":
+            for key, att, win, slot in step["probe"]:
+                _, stats = t.retrieve_with_stats(int(key))
+                assert (stats.attempts, stats.windows_visited) == (att, win), key
+                assert t.slot_of(int(key)) == slot, key
+    keys = [t.slots.load_key(i) for i in range(t.capacity)]
+    vals = [t.slots.load_value(i) for i in range(t.capacity)]
+    assert keys == ints(sc["final_keys"])
+    assert vals == ints(sc["final_vals"])
+    assert (t.occupied, t.tombstones) == (sc["occupied"], sc["tombstones"])
+    c = t.probe_counters()
+    assert (c.ops, c.attempts, c.windows_visited) == \
+        (sc["counters"]["ops"], sc["counters"]["attempts"], sc["counters"]["windows"])
+
+
+# ------------------------------------------------ bulk replay: semantic parity
+
+@pytest.mark.parametrize("idx", range(11))
+def test_bulk_replay_semantics(idx):
+    sc = load("single.json")["scenarios"][idx]
+    t = table_from(sc)
+    model: dict[int, int] = {}
+    any_full = False
+    for step in sc["steps"]:
+        if step["op"] == "insert_bulk":
+            keys, vals = ints(step["keys"]), ints(step["vals"])
+            got = t.insert_bulk(list(zip(keys, vals)))
+            ref = step["status"]
+            any_full |= "table_full" in ref or InsertStatus.TABLE_FULL in got
+            mult = Counter(keys)
+            winners = {}
+            for k, v, g, r in zip(keys, vals, got, ref):
+                if r == "invalid_key":
+                    assert g == InsertStatus.INVALID_KEY
+                elif mult[k] == 1 and not any_full:
+                    assert g.value == r, k  # distinct keys: exact status
+                if g == INSERTED:
+                    assert k not in winners, "two INSERTED for one key"
+                    winners[k] = v
+            if not any_full:
+                new_keys = {k for k, r in zip(keys, ref) if r == "inserted"}
+                assert set(winners) == new_keys, "new keys must be inserted exactly once"
+            model.update(winners)
+        elif step["op"] == "erase":
+            keys = ints(step["keys"])
+            er = t.erase_device(keys).cpu().numpy().astype(bool).tolist()
+            # a key listed twice is retired once, by either position
+            assert Counter(k for k, hit in zip(keys, er) if hit) == \
+                Counter(k for k, hit in zip(keys, step["result"]) if hit) or any_full
+            for k, hit in zip(keys, er):
+                if hit:
+                    model.pop(k)
+        elif step["op"] == "retrieve_bulk":
+            keys = ints(step["keys"])
+            assert t.retrieve_bulk(keys) == [model.get(k) for k in keys]
+    assert {k: v for _, k, v in t.slots.iter_items()} == model
+    if not any_full:
+        assert t.occupied == sc["occupied"]
+
+
+# ------------------------------------------------ large batches vs the oracle
+
+@pytest.mark.parametrize("layout,kb,vb,g", [
+    ("packed", 32, 32, 1), ("packed", 32, 32, 2), ("packed", 32, 32, 4), ("packed", 32, 32, 8),
+    ("packed", 32, 32, 16), ("packed", 32, 32, 32),
+    ("soa", 64, 64, 4), ("soa", 32, 64, 8), ("soa", 64, 32, 16), ("soa", 32, 32, 32),
+    ("aos", 64, 64, 8), ("aos", 32, 32, 4), ("aos", 32, 64, 2), ("aos", 64, 32, 1),
+])
+@pytest.mark.parametrize("rho", [0.8, 0.95])
+def test_bulk_unique_vs_oracle(layout, kb, vb, g, rho):
+    n = 1 << 18
+    rng = np.random.default_rng(zlib.crc32(f"{layout}{kb}{vb}{g}{rho}".encode()))
+    hi = (1 << kb) - 3
+    keys = rng.permutation(np.unique(rng.integers(1, hi, size=3 * n, dtype=np.uint64)))
+    present, absent = keys[:n], keys[n:2 * n]
+    vals = rng.integers(0, (1 << vb) - 1, size=n, dtype=np.uint64)
+    cap = int(np.ceil(n / rho))
+    t = SingleValueHashTable(cap, layout=layout, key_bits=kb, value_bits=vb, group_width=g)
+    st = t.insert_device(present, vals).cpu().numpy()
+    assert (st == 0).all()
+    assert t.occupied == n
+    v, f = t.retrieve_device(present)
+    assert f.cpu().numpy().all()
+    got = v.cpu().numpy().view(np.uint32 if vb <= 32 else np.uint64).astype(np.uint64)
+    assert (got == vals).all()
+    v2, f2 = t.retrieve_device(absent)
+    assert not f2.cpu().numpy().any()
+    assert (v2.cpu().numpy() == 0).all()
+    # re-inserting is all duplicates and leaves the values untouched
+    st2 = t.insert_device(present, vals ^ np.uint64(1)).cpu().numpy()
+    assert (st2 == 1).all()
+    # the oracle agrees on occupancy and the hit/miss sets
+    ref = orc.OracleSingle(cap, group_width=g, key_bits=kb, packed=layout == "packed")
+    ref.insert_bulk(present, vals)
+    assert ref.stats()["occupied"] == t.occupied
+    rv, rf = ref.retrieve_bulk(present[:4096])
+    assert (rv == got[:4096]).all() and rf.all()
+
+
+def test_retrieve_probe_counts_match_oracle_readonly():
+    """Read-only probes are schedule independent: mean attempts equal the oracle's."""
+    n = 1 << 16
+    rng = np.random.default_rng(3)
+    keys = rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=2 * n, dtype=np.uint64)))[:n]
+    for g in (1, 4, 32):
+        t = SingleValueHashTable(int(n / 0.9), layout="packed", key_bits=32, value_bits=32, group_width=g)
+        ref = orc.OracleSingle(int(n / 0.9), group_width=g, key_bits=32, packed=True)
+        # sequentially-equivalent placement: insert the oracle's final state directly
+        ref.insert_bulk(keys, keys)
+        rk, rvals = ref.dump()
+        t._dt  # noqa: B018
+        from paper_2009_07914_b200 import _lib
+        k32 = rk.astype(np.uint32)
+        v32 = rvals.astype(np.uint32)
+        _lib.check(_lib.lib().ch_write_slots(t._dt.handle, k32.ctypes.data, v32.ctypes.data))
+        t._dt.touch()
+        before = ref.stats()
+        t.reset_probe_counters()
+        t.retrieve_device(keys)
+        ref.retrieve_bulk(keys)
+        after = ref.stats()
+        c = t.probe_counters()
+        assert c.ops == after["ops"] - before["ops"]
+        assert c.attempts == after["attempts"] - before["attempts"]
+        assert c.windows_visited == after["windows"] - before["windows"]
+
+
+# ------------------------------------------------ reference test_single_table.py mirrors
+
+def _table(min_capacity=1000, **kw):
+    return SingleValueHashTable(min_capacity, **kw)
+
+
+def test_singleton_and_duplicate():          # test_single_table.py:19-31
+    t = _table()
+    assert t.insert(5, 50) == INSERTED
+    assert t.retrieve(5) == 50 and t.occupied == 1
+    assert t.insert(5, 51) == DUP and t.retrieve(5) == 50
+
+
+def test_invalid_key_rejected():             # :34-40
+    t = _table()
+    e = t.slots.sentinels.empty_key
+    assert t.insert(e, 1) == InsertStatus.INVALID_KEY
+    assert t.insert(t.slots.sentinels.tombstone_key, 1) == InsertStatus.INVALID_KEY
+    assert t.retrieve(e) is None and not t.erase(e)
+
+
+def test_fill_to_high_density():             # :43-50
+    t = _table(1000)
+    n = int(t.capacity * 0.97)
+    st = t.insert_bulk([(k, k + 1) for k in range(1, n + 1)])
+    assert all(s == INSERTED for s in st)
+    assert t.retrieve_bulk(range(1, n + 1)) == [k + 1 for k in range(1, n + 1)]
+    assert t.load_factor() == n / t.capacity
+
+
+def test_absent_key_stops_after_first_window():  # :53-58
+    t = _table()
+    value, stats = t.retrieve_with_stats(12345)
+    assert value is None and stats.windows_visited == 1 and stats.attempts >= 1
+
+
+def test_erase_semantics():                  # :61-85
+    t = _table()
+    assert not t.erase(4)
+    t.insert(4, 44)
+    assert t.erase(4) and not t.erase(4)
+    assert t.retrieve(4) is None
+    t.insert(6, 60)
+    before, slot = t.occupied, t.slot_of(6)
+    assert t.erase(6)
+    assert t.insert(6, 61) == INSERTED
+    assert t.occupied == before and t.slot_of(6) == slot and t.retrieve(6) == 61
+
+
+def _colliding_pair(table):
+    cfg = table.config
+    seen = {}
+    for key in range(1, 1 << 20):
+        start = cfg.hash.value(key) % cfg.plan.c
+        if start in seen:
+            return seen[start], key
+        seen[start] = key
+    raise AssertionError
+
+
+def test_tombstone_cases():                  # :101-124
+    t = _table()
+    k1, k2 = _colliding_pair(t)
+    t.insert(k1, 100)
+    t.erase(k1)
+    assert t.insert(k2, 200) == INSERTED and t.retrieve(k2) == 200
+    assert sum(1 for _, k, _ in t.slots.iter_items() if k == k2) == 1
+    t2 = _table()
+    t2.insert(k1, 1)
+    t2.insert(k2, 2)
+    t2.erase(k1)
+    assert t2.insert(k2, 3) == DUP and t2.retrieve(k2) == 2
+    # same in one concurrent batch: the duplicate behind the tombstone is still found
+    assert t2.insert_bulk([(k2, 4)] * 64) == [DUP] * 64
+
+
+def test_lowest_index_placement():           # :127-142
+    import random
+    t = _table(3000)
+    rng = random.Random(41)
+    keys = rng.sample(range(1, 1 << 30), 2000)
+    t.insert_bulk([(k, k) for k in keys])  # concurrent: still no empty before any key
+    e = t.slots.sentinels.empty_key
+    for k in rng.sample(keys, 200):
+        for idx in probing.probe_order(k, t.config):
+            cell = t.slots.load_key(idx)
+            if cell == k:
+                break
+            assert cell != e
+        else:
+            raise AssertionError
+
+
+@pytest.mark.parametrize("layout,key_bits,ops", [(LayoutKind.SOA, 64, 3000), (LayoutKind.AOS, 64, 2000),
+                                                 (LayoutKind.PACKED_AOS, 32, 2000)])
+def test_oracle_equivalence_random_ops(layout, key_bits, ops):   # :145-175
+    import random
+    t = SingleValueHashTable(256, layout=layout, key_bits=key_bits,
+                             value_bits=32 if layout == LayoutKind.PACKED_AOS else 64)
+    domain = int(t.capacity * 0.7)
+    rng = random.Random(97)
+    ref = {}
+    for step in range(ops):
+        key = rng.randrange(1, domain)
+        roll = rng.random()
+        if roll < 0.5:
+            value = rng.randrange(1, 1 << 30)
+            st = t.insert(key, value)
+            assert st == (DUP if key in ref else INSERTED), step
+            ref.setdefault(key, value)
+        elif roll < 0.8:
+            assert t.retrieve(key) == ref.get(key), step
+        else:
+            assert t.erase(key) == (ref.pop(key, None) is not None), step
+    assert {k: v for _, k, v in t.slots.iter_items()} == ref
+    assert t.occupied == len(ref)
+
+
+def test_in_batch_duplicates():              # :190-197
+    t = _table(1000)
+    st = t.insert_bulk([(5, 1), (6, 2), (5, 3), (5, 4), (6, 5)])
+    assert st.count(INSERTED) == 2 and st.count(DUP) == 3
+    assert t.retrieve(5) in (1, 3, 4) and t.retrieve(6) in (2, 5)
+
+
+def test_same_key_storm_single_winner():     # :278-298 (8 threads -> 1M lanes)
+    t = SingleValueHashTable(256, layout="packed", key_bits=32, value_bits=32)
+    n = 1 << 20
+    keys = torch.full((n,), 777, dtype=torch.int32, device="cuda")
+    vals = torch.arange(n, dtype=torch.int32, device="cuda")
+    st = t.insert_device(keys, vals).cpu().numpy()
+    assert (st == 0).sum() == 1 and (st == 1).sum() == n - 1
+    assert t.retrieve(777) == int(np.nonzero(st == 0)[0][0])
+    assert t.occupied == 1
+
+
+def test_empty_and_load_factor():            # :200-231
+    t = _table(1000)
+    assert t.insert_bulk([]) == [] and t.retrieve_bulk([]) == []
+    assert t.load_factor() == 0.0
+    t.insert_bulk([(k, k) for k in range(1, 11)])
+    assert t.load_factor() == 10 / t.capacity
+    t.erase(1)
+    assert t.load_factor() == 9 / t.capacity and t.tombstones == 1
+
+
+def test_table_full_after_whole_cycle():     # :234-239
+    t = _table(32)
+    for k in range(1, 65):
+        assert t.insert(k, k) == INSERTED
+    assert t.insert(999, 1) == InsertStatus.TABLE_FULL
+    assert t.load_factor() == 1.0
+    b = _table(32)
+    st = b.insert_bulk([(k, k) for k in range(1, 66)])
+    assert st.count(INSERTED) == 64 and st.count(InsertStatus.TABLE_FULL) == 1
+
+
+def test_group_widths_agree_on_final_state():  # :242-252
+    import random
+    rng = random.Random(61)
+    keys = rng.sample(range(1, 1 << 30), 500)
+    views = []
+    for g in (1, 2, 4, 8, 16, 32):
+        t = _table(1000, group_width=g)
+        for k in keys:
+            t.insert(k, k + 1)
+        t.erase(keys[0])
+        views.append({k: v for _, k, v in t.slots.iter_items()})
+    assert all(v == views[0] for v in views)
+
+
+def test_for_each_and_for_all():             # :206-220
+    t = _table()
+    items = {k: k * 7 for k in range(1, 101)}
+    t.insert_bulk(list(items.items()))
+    seen = {}
+    t.for_all(lambda k, v, i: seen.__setitem__(k, v))
+    assert seen == items
+    hits = []
+    t.for_each([1, 2, 999_999], lambda k, v, i: hits.append((k, v)))
+    assert hits == [(1, 7), (2, 14)]
+
+
+def test_find_or_claim():
+    t = _table()
+    st, slot = t.find_or_claim(42)
+    assert st == INSERTED and slot == t.slot_of(42)
+    st2, slot2 = t.find_or_claim(42)
+    assert st2 == DUP and slot2 == slot
