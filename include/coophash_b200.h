@@ -74,6 +74,8 @@ typedef struct ch_stats {
 
 const char* ch_last_error(void);
 int ch_version(void);
+/* number of CUDA kernels this library has launched (process-wide counter) */
+uint64_t ch_kernel_launches(void);
 
 /* ---- lifetime ---- replaces SingleValueHashTable/MultiValueHashTable/BucketListHashTable
  * construction (single_table.py:91-114, multi_table.py:36-58, bucket_list.py:167-188).
@@ -84,6 +86,9 @@ int ch_clear(ch_table* t, void* stream);               /* K0: every cell empty, 
 int ch_get_stats(ch_table* t, ch_stats* out);          /* synchronizes the table's work */
 int ch_reset_probe_counters(ch_table* t, void* stream); /* single_table.py:136-138 */
 int ch_synchronize(ch_table* t);
+/* region-ordered execution of big batches (csrc/locality.cu): 0 auto (table > 256 MiB and
+ * n >= c/16), 1 never, 2 always.  Results are identical; only the schedule changes. */
+int ch_set_locality(ch_table* t, int mode);
 
 /* ---- single-value (and bucket key store) ---- */
 /* insert_bulk (single_table.py:355-374): d_status[n] */

@@ -41,12 +41,14 @@ _U64 = C.c_uint64
 _SIGS = {
     "ch_last_error": (C.c_char_p, []),
     "ch_version": (C.c_int, []),
+    "ch_kernel_launches": (C.c_uint64, []),
     "ch_create": (C.c_int, [C.POINTER(_P), C.POINTER(ch_config)]),
     "ch_destroy": (C.c_int, [_P]),
     "ch_clear": (C.c_int, [_P, _P]),
     "ch_get_stats": (C.c_int, [_P, C.POINTER(ch_stats)]),
     "ch_reset_probe_counters": (C.c_int, [_P, _P]),
     "ch_synchronize": (C.c_int, [_P]),
+    "ch_set_locality": (C.c_int, [_P, C.c_int]),
     "ch_insert": (C.c_int, [_P, _P, _P, _U64, _P, _P]),
     "ch_find_or_claim": (C.c_int, [_P, _P, _U64, _P, _P, _P]),
     "ch_retrieve": (C.c_int, [_P, _P, _U64, _P, _P, _P]),

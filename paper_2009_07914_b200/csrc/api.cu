@@ -4,6 +4,7 @@
 // previous one (a per-table event), validates configurations the way the
 // reference constructors do, and turns CUDA errors into negative codes with a
 // thread-local message.  No exception crosses the ABI.
+#include <atomic>
 #include <cerrno>
 #include <cstdio>
 #include <cstring>
@@ -20,6 +21,8 @@ namespace chb {
 
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // prims.cu / bucket.cu entry points
 int mix64_array(const Launch& lc, const uint64_t* in, uint64_t n, uint64_t seed, uint64_t* out);
@@ -36,6 +39,18 @@ int bucket_insert(const Launch& lc, const BucketRef& B, const TypeSel& ts, const
                   uint64_t n, uint8_t* status, int64_t* slots, uint32_t* rank, uint64_t* need, uint64_t* alloc_off,
                   void* scan_scratch, size_t scan_bytes);
 int bucket_counts(const Launch& lc, const uint64_t* handles, uint64_t n, uint32_t* counts);
+struct LocPlan {
+  int shift;
+  uint32_t regions;
+  uint64_t tiles;
+};
+LocPlan loc_plan(const TableRef& T, uint64_t n, int bytes_per_slot);
+size_t loc_scratch_bytes(const LocPlan& p);
+int loc_partition(const Launch& lc, const TableRef& T, const LocPlan& p, int kbytes, int vbytes, const void* keys,
+                  const void* vals, uint64_t n, void* keys_out, void* vals_out, uint16_t* inv, void* scratch,
+                  size_t scratch_bytes);
+int loc_unpermute(const Launch& lc, const LocPlan& p, uint64_t n, const uint16_t* inv, void* scratch,
+                  size_t scratch_bytes, const void* pa, void* oa, int abytes, const void* pb, void* ob, int bbytes);
 int bucket_walk(const Launch& lc, const BucketRef& B, int vbytes, const uint64_t* handles, uint64_t n,
                 const uint64_t* offsets, void* out);
 
@@ -62,6 +77,7 @@ struct ch_table {
   cudaEvent_t last = nullptr;
   std::mutex mu;
   int sms = 148;
+  int loc_mode = 0;  // 0 auto, 1 never, 2 always (region-ordered execution, locality.cu)
 };
 
 namespace {
@@ -152,6 +168,30 @@ BucketRef bucket_ref(ch_table* t) {
   return B;
 }
 
+int slot_bytes_of(const ch_table* t) {
+  if (t->cfg.layout == CH_PACKED) return 8;
+  const int kb = t->ts.kbytes, vb = t->ts.vbytes;
+  if (t->cfg.layout == CH_SOA) return kb + vb;
+  return (kb == 8 || vb == 8) ? 16 : 8;
+}
+
+// Region-ordered execution pays off once the table outgrows L2 and the batch
+// touches most of its lines (locality.cu).  Positions travel as uint32.
+bool use_locality(const ch_table* t, uint64_t n) {
+  if (n == 0 || n >= (1ull << 32) || t->loc_mode == 1) return false;
+  if (t->loc_mode == 2) return true;
+  const uint64_t bytes = t->T.c * (uint64_t)slot_bytes_of(t);
+  return bytes >= (256ull << 20) && n * 16 >= t->T.c;
+}
+
+void keep_pool_memory(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
 __global__ void k_zero_counters(DevCounters* c) { *c = DevCounters{}; }
 
 __global__ void k_reset_probe(DevCounters* c) {
@@ -218,6 +258,7 @@ __global__ void k_slot_op(TableRef T, int layout, int op, uint64_t slot, uint64_
 extern "C" {
 
 const char* ch_last_error(void) { return g_err.c_str(); }
+uint64_t ch_kernel_launches(void) { return g_launches.load(); }
 int ch_version(void) { return 1; }
 
 int ch_create(ch_table** out, const ch_config* cfg) {
@@ -234,6 +275,7 @@ int ch_create(ch_table** out, const ch_config* cfg) {
     return fail(CH_EINVAL, "list handles need 64-bit value cells; use the soa or aos layout");
   if (!pow2_group(c.group_width)) return fail(CH_EINVAL, "group_width must be one of (1, 2, 4, 8, 16, 32)");
   if (c.p < 2) return fail(CH_EINVAL, "window count p must be a prime >= 2");
+  if (c.p >= (1ull << 32)) return fail(CH_EINVAL, "window count p must be < 2^32 (capacity < 2^37 slots)");
   const uint64_t maxw = c.max_outer_attempts ? c.max_outer_attempts : c.p;
   if (maxw < 1 || maxw > c.p) return fail(CH_EINVAL, "max_outer_attempts must be in [1, p]");
   if (c.empty_key == c.tombstone_key) return fail(CH_EINVAL, "empty and tombstone sentinels must differ");
@@ -288,8 +330,9 @@ int ch_create(ch_table** out, const ch_config* cfg) {
   if (cudaMalloc(&T.slots, t->slot_bytes) != cudaSuccess) return cleanup(CH_ENOMEM, "slot array allocation failed");
   if (t->val_bytes && cudaMalloc(&T.vals, t->val_bytes) != cudaSuccess)
     return cleanup(CH_ENOMEM, "value array allocation failed");
-  if (cudaMalloc(&t->ctr, sizeof(DevCounters)) != cudaSuccess) return cleanup(CH_ENOMEM, "counter allocation failed");
+  if (cudaMalloc(&t->ctr, sizeof(DevCounters) + 64) != cudaSuccess) return cleanup(CH_ENOMEM, "counter allocation failed");
   T.ctr = t->ctr;
+  T.work = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(t->ctr) + sizeof(DevCounters));
 
   if (c.kind == CH_BUCKET) {
     std::vector<uint64_t> sizes, sums;
@@ -305,6 +348,7 @@ int ch_create(ch_table** out, const ch_config* cfg) {
         cudaMemcpy(t->gsums, sums.data(), t->gm * 8, cudaMemcpyHostToDevice) != cudaSuccess)
       return cleanup(CH_EIO, "growth table upload failed");
   }
+  keep_pool_memory(c.device);
   int rc = ch_clear(t, nullptr);
   if (rc) {
     std::string m = g_err;
@@ -339,6 +383,7 @@ int ch_clear(ch_table* t, void* stream) {
   int rc = single_clear(o.lc, t->T, t->ts);
   if (!rc) {
     k_zero_counters<<<1, 1, 0, o.s>>>(t->ctr);
+    count_launch();
     rc = check(cudaGetLastError(), "zero counters");
   }
   if (!rc && t->cfg.kind == CH_BUCKET) {
@@ -348,6 +393,13 @@ int ch_clear(ch_table* t, void* stream) {
   }
   t->host_ops = 0;
   return o.done(rc);
+}
+
+int ch_set_locality(ch_table* t, int mode) {
+  if (!t || mode < 0 || mode > 2) return fail(CH_EINVAL, "locality mode must be 0 (auto), 1 (off) or 2 (on)");
+  std::lock_guard<std::mutex> lock(t->mu);
+  t->loc_mode = mode;
+  return CH_OK;
 }
 
 int ch_synchronize(ch_table* t) {
@@ -381,6 +433,7 @@ int ch_reset_probe_counters(ch_table* t, void* stream) {
   if (!t) return fail(CH_EINVAL, "null table");
   Ordered o(t, stream);
   k_reset_probe<<<1, 1, 0, o.s>>>(t->ctr);
+  count_launch();
   t->host_ops = 0;
   return o.done(check(cudaGetLastError(), "reset counters"));
 }
@@ -390,7 +443,21 @@ int ch_insert(ch_table* t, const void* keys, const void* vals, uint64_t n, uint8
   if (t->cfg.kind != CH_SINGLE) return fail(CH_EINVAL, "ch_insert needs a single-value table");
   if (n && (!keys || !vals || !status)) return fail(CH_EINVAL, "null buffer");
   Ordered o(t, stream);
-  return o.done(single_insert(o.lc, t->T, t->ts, keys, vals, n, status, nullptr, 0));
+  if (!use_locality(t, n)) return o.done(single_insert(o.lc, t->T, t->ts, keys, vals, n, status, nullptr, 0));
+  const LocPlan p = loc_plan(t->T, n, slot_bytes_of(t));
+  Scratch sc(o.s);
+  const int kb = t->ts.kbytes, vb = t->ts.vbytes;
+  void* kp = sc.get(n * kb);
+  void* vp = sc.get(n * vb);
+  uint16_t* inv = (uint16_t*)sc.get(n * 2);
+  uint8_t* sp = (uint8_t*)sc.get(n);
+  const size_t lb = loc_scratch_bytes(p);
+  void* ls = sc.get(lb);
+  if (!kp || !vp || !inv || !sp || !ls) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+  int rc = loc_partition(o.lc, t->T, p, kb, vb, keys, vals, n, kp, vp, inv, ls, lb);
+  if (!rc) rc = single_insert(o.lc, t->T, t->ts, kp, vp, n, sp, nullptr, 0);
+  if (!rc) rc = loc_unpermute(o.lc, p, n, inv, ls, lb, sp, status, 1, nullptr, nullptr, 0);
+  return o.done(rc);
 }
 
 int ch_find_or_claim(ch_table* t, const void* keys, uint64_t n, uint8_t* status, int64_t* slots, void* stream) {
@@ -406,7 +473,22 @@ int ch_retrieve(ch_table* t, const void* keys, uint64_t n, void* vals_out, uint8
   if (t->cfg.kind != CH_SINGLE) return fail(CH_EINVAL, "ch_retrieve needs a single-value table");
   if (n && (!keys || !vals_out || !found)) return fail(CH_EINVAL, "null buffer");
   Ordered o(t, stream);
-  return o.done(single_lookup(o.lc, t->T, t->ts, keys, n, vals_out, found, nullptr, nullptr, nullptr, 0));
+  if (!use_locality(t, n))
+    return o.done(single_lookup(o.lc, t->T, t->ts, keys, n, vals_out, found, nullptr, nullptr, nullptr, 0));
+  const LocPlan p = loc_plan(t->T, n, slot_bytes_of(t));
+  Scratch sc(o.s);
+  const int kb = t->ts.kbytes, vb = t->ts.vbytes;
+  void* kp = sc.get(n * kb);
+  uint16_t* inv = (uint16_t*)sc.get(n * 2);
+  void* vp = sc.get(n * vb);
+  uint8_t* fp = (uint8_t*)sc.get(n);
+  const size_t lb = loc_scratch_bytes(p);
+  void* ls = sc.get(lb);
+  if (!kp || !vp || !inv || !fp || !ls) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+  int rc = loc_partition(o.lc, t->T, p, kb, vb, keys, nullptr, n, kp, nullptr, inv, ls, lb);
+  if (!rc) rc = single_lookup(o.lc, t->T, t->ts, kp, n, vp, fp, nullptr, nullptr, nullptr, 0);
+  if (!rc) rc = loc_unpermute(o.lc, p, n, inv, ls, lb, vp, vals_out, vb, fp, found, 1);
+  return o.done(rc);
 }
 
 int ch_erase(ch_table* t, const void* keys, uint64_t n, uint8_t* erased, void* stream) {
@@ -586,6 +668,7 @@ int ch_slot_op(ch_table* t, int op, uint64_t slot, uint64_t expected, uint64_t d
   else if (kb == 4) k_slot_op<uint32_t, uint64_t><<<1, 1, 0, o.s>>>(t->T, t->cfg.layout, op, slot, expected, desired, value, d);
   else if (vb == 4) k_slot_op<uint64_t, uint32_t><<<1, 1, 0, o.s>>>(t->T, t->cfg.layout, op, slot, expected, desired, value, d);
   else k_slot_op<uint64_t, uint64_t><<<1, 1, 0, o.s>>>(t->T, t->cfg.layout, op, slot, expected, desired, value, d);
+  count_launch();
   int rc = check(cudaGetLastError(), "slot op");
   unsigned long long hbuf[3] = {0, 0, 0};
   if (!rc) rc = check(cudaMemcpyAsync(hbuf, d, 24, cudaMemcpyDeviceToHost, o.s), "slot op read");

@@ -279,6 +279,7 @@ int bucket_insert(const Launch& lc, const BucketRef& B, const TypeSel& ts, const
   if (rc) return rc;
   if (k4) k_bucket_alloc_seq<uint32_t><<<1, 32, 0, lc.stream>>>(B, lay, alloc_off, ts.vbytes);
   else k_bucket_alloc_seq<uint64_t><<<1, 32, 0, lc.stream>>>(B, lay, alloc_off, ts.vbytes);
+  count_launch();
   rc = cuda_check(cudaGetLastError(), "bucket alloc seq");
   if (rc) return rc;
   if (ts.vbytes == 8) {

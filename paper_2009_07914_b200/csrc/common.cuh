@@ -82,6 +82,7 @@ struct TableRef {
   uint64_t e, t;    // sentinels
   FastMod modc, modpm1;
   DevCounters* ctr;
+  unsigned long long* work;  // chunk queue of the running probe kernel (sched.cuh)
 };
 
 struct ProbeStart {
@@ -131,11 +132,17 @@ template <> __device__ __forceinline__ Vec<32> ld_cg<32>(const void* p) {
   return v;
 }
 
-// streaming (evict-first) loads/stores for the batch inputs and outputs
+// Batch inputs / outputs.  Probe groups consume keys and emit results at
+// different times (each resolves its key after a different number of steps),
+// so neighbouring elements of one 128 B line are touched by many warps over a
+// short interval.  Evict-first (.cs) hints made L2 drop such lines between
+// touches -- every 4 B key re-fetched a 128 B line and every 1-4 B result
+// became a DRAM read-modify-write (profiles/r01_launches_loc_v1.csv).  Default
+// caching lets L2 merge them: one line fill / write-back per 128 B.
 template <typename X>
-__device__ __forceinline__ X ld_stream(const X* p) { return __ldcs(p); }
+__device__ __forceinline__ X ld_stream(const X* p) { return __ldg(p); }
 template <typename X>
-__device__ __forceinline__ void st_stream(X* p, X v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(X* p, X v) { *p = v; }
 
 __device__ __forceinline__ uint32_t atomic_cas(uint32_t* p, uint32_t cmp, uint32_t val) {
   return atomicCAS(reinterpret_cast<unsigned int*>(p), cmp, val);

@@ -47,6 +47,9 @@ inline int occupancy(const void* kern, int threads) {
   return occ;
 }
 
+// Kernel launches issued by this library (bench.py reports them per timed region).
+void count_launch(uint64_t n = 1);
+
 // Persistent grid: one wave of CTAs (SMs x resident CTAs/SM), or fewer for
 // small batches; kernels grid-stride over items.
 template <typename F>
@@ -57,6 +60,23 @@ int launch_persistent(const Launch& lc, const void* kern, uint64_t items, int la
   const uint64_t full = (uint64_t)lc.sms * (uint64_t)occupancy(kern, threads);
   const uint64_t blocks = want < full ? want : full;
   fn(dim3((unsigned)blocks), dim3(threads));
+  count_launch();
+  return cuda_check(cudaGetLastError(), "kernel launch");
+}
+
+// Chunk-scheduled probe kernels (sched.cuh): reset the table's work queue,
+// then one wave of CTAs (no more CTAs than chunks).
+template <typename F>
+int launch_chunked(const Launch& lc, const TableRef& T, const void* kern, uint64_t items, int chunk, F&& fn,
+                   int threads = 256) {
+  if (items == 0) return 0;
+  int rc = cuda_check(cudaMemsetAsync(T.work, 0, sizeof(unsigned long long), lc.stream), "queue reset");
+  if (rc) return rc;
+  const uint64_t want = (items + chunk - 1) / chunk;
+  const uint64_t full = (uint64_t)lc.sms * (uint64_t)occupancy(kern, threads);
+  const uint64_t blocks = want < full ? want : full;
+  fn(dim3((unsigned)blocks), dim3(threads));
+  count_launch();
   return cuda_check(cudaGetLastError(), "kernel launch");
 }
 

@@ -98,6 +98,7 @@ static int scan_impl(const Launch& lc, const TIn* in, uint64_t n, uint64_t* out,
   const uint64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (tiles == 1) {
     k_tile_scan<TIn><<<1, SCAN_THREADS, 0, lc.stream>>>(in, n, nullptr, out);
+    count_launch();
     return cuda_check(cudaGetLastError(), "scan");
   }
   if (scratch_words < tiles + 1) {
@@ -107,6 +108,7 @@ static int scan_impl(const Launch& lc, const TIn* in, uint64_t n, uint64_t* out,
   uint64_t* sums = scratch;  // tiles sums, then scanned in place into sums_scan
   uint64_t* sums_scan = scratch + 0;
   k_tile_sums<TIn><<<(unsigned)tiles, SCAN_THREADS, 0, lc.stream>>>(in, n, sums);
+  count_launch();
   int rc = cuda_check(cudaGetLastError(), "scan sums");
   if (rc) return rc;
   // scan the tile sums (recursively) into the scratch area that follows them
@@ -115,6 +117,7 @@ static int scan_impl(const Launch& lc, const TIn* in, uint64_t n, uint64_t* out,
   if (rc) return rc;
   (void)sums_scan;
   k_tile_scan<TIn><<<(unsigned)tiles, SCAN_THREADS, 0, lc.stream>>>(in, n, next, out);
+  count_launch();
   return cuda_check(cudaGetLastError(), "scan tiles");
 }
 
@@ -249,6 +252,7 @@ static int split_impl(const Launch& lc, const K* keys, const V* vals, uint64_t n
   const uint64_t tiles = (n + SPLIT_TILE - 1) / SPLIT_TILE;
   if (n == 0) {
     k_split_offsets<<<1, 256, 0, lc.stream>>>(nullptr, shards, 0, 0, offsets);
+    count_launch();
     return cuda_check(cudaGetLastError(), "split offsets");
   }
   const uint64_t h = tiles * shards;
@@ -261,15 +265,18 @@ static int split_impl(const Launch& lc, const K* keys, const V* vals, uint64_t n
     return -22;
   }
   k_split_count<K><<<(unsigned)tiles, SPLIT_THREADS, 0, lc.stream>>>(keys, n, shards, hist);
+  count_launch();
   int rc = cuda_check(cudaGetLastError(), "split count");
   if (rc) return rc;
   rc = exclusive_scan_u32(lc, hist, h, hist_off, scan_scratch, scratch_bytes - used);
   if (rc) return rc;
   k_split_scatter<K, V><<<(unsigned)tiles, SPLIT_THREADS, 0, lc.stream>>>(keys, vals, n, shards, hist_off, perm,
                                                                          keys_out, vals_out);
+  count_launch();
   rc = cuda_check(cudaGetLastError(), "split scatter");
   if (rc) return rc;
   k_split_offsets<<<1, 256, 0, lc.stream>>>(hist_off, shards, tiles, n, offsets);
+  count_launch();
   return cuda_check(cudaGetLastError(), "split offsets");
 }
 

@@ -1,11 +1,22 @@
 // probe.cuh -- the COPS probe step shared by every table kernel.
 //
-// One step: the group loads the aligned span containing the next unexamined
-// slot of the key's sequence, and reduces three group-uniform bit masks over
-// the span (bit u <=> slot base+u): key matches, empties and tombstones,
-// restricted to the slots that belong to the current window at or after the
-// cursor.  Callers decide in sequence order (lowest bit first), which is the
-// reference's lowest-index-first rule (single_table.py:198-223).
+// One step: the prober loads the aligned span containing the next unexamined
+// slot of its key's sequence and builds three bit masks over the span (bit u
+// <=> slot base+u): key matches, empties and tombstones, restricted to the
+// slots that belong to the current window at or after the cursor.  Callers
+// decide in sequence order (lowest bit first), which is the reference's
+// lowest-index-first rule (single_table.py:198-223).
+//
+// B200 mapping.  The paper probes with a cooperative group of g lanes, one
+// slot per lane, combined by ballots.  A B200 thread can issue 256-bit loads,
+// so here ONE thread owns a key and loads the whole span itself with up to
+// four 32 B vector loads issued back to back (one memory latency per step).
+// There is no cross-lane reduction at all: on sm_100a the tile shuffles of
+// divergent probe groups compiled to ~150 SHFL + 50 WARPSYNC.COLLECTIVE per
+// loop body (profiles/r01_sass_tile_shuffles.txt).  The span is group_width
+// slots capped at 128 B; the reference's per-g probe counters stay exact
+// because they are computed from sequence positions (chunk_end), not from the
+// hardware span.
 #pragma once
 #include "common.cuh"
 
@@ -13,46 +24,68 @@ namespace chb {
 
 template <Layout LAY, typename K, typename V, int G>
 struct Probe {
-  using Geo = Geometry<LAY, K, V, G>;
-  using Ops = typename Geo::Ops;
-  static constexpr int SPL = Geo::SPL;
-  static constexpr int L = Geo::L;
-  static constexpr int A = Geo::A;
+  using Ops = LayoutOps<LAY, K, V>;
+  static constexpr int A_MAX = 128 / Ops::UNIT > 0 ? 128 / Ops::UNIT : 1;
+  static constexpr int A = G < A_MAX ? G : A_MAX;                   // slots per step (power of 2, divides 32)
+  static constexpr int SPL = A < Ops::SPL_MAX ? A : Ops::SPL_MAX;   // slots per vector load
+  static constexpr int NV = A / SPL;                                // vector loads per step
+  static constexpr int L = 1;
   using Slots = typename Ops::template Slots<SPL>;
+  static_assert(SPL * NV == A && A >= 1 && A <= 32 && (32 % A) == 0, "bad span");
 
   struct Step {
     uint64_t base;   // aligned span start slot
     uint32_t lo;     // first useful bit
     uint32_t n_use;  // useful bits
     uint32_t km, em, tm;
-    Slots sl;        // this lane's SPL slots
+    Slots sl[NV];
   };
 
-  template <typename Tile>
-  __device__ __forceinline__ static void load(const TableRef& T, const Tile& tile, const Cursor& cur,
-                                              K key, Step& st) {
+  __device__ __forceinline__ static void load(const TableRef& T, const Cursor& cur, K key, Step& st) {
     const uint64_t q = cur.slot(T);
     st.base = q & ~(uint64_t)(A - 1);
     st.lo = (uint32_t)(q - st.base);
     const uint32_t room = WINDOW - cur.o;
     st.n_use = (A - st.lo) < room ? (A - st.lo) : room;
     const uint32_t hi = st.lo + st.n_use;
-    const int lane = L > 1 ? (int)tile.thread_rank() : 0;
-    st.sl = Ops::template load<SPL>(T, st.base + (uint64_t)lane * SPL);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) st.sl[v] = Ops::template load<SPL>(T, st.base + (uint64_t)v * SPL);
     uint32_t km = 0, em = 0, tm = 0;
     const K e = (K)T.e, t = (K)T.t;
 #pragma unroll
-    for (int s = 0; s < SPL; ++s) {
-      const uint32_t u = (uint32_t)(lane * SPL + s);
-      const bool in = u >= st.lo && u < hi;
-      const K k = st.sl.key(s);
-      km |= (uint32_t)(in && k == key) << u;
-      em |= (uint32_t)(in && k == e) << u;
-      tm |= (uint32_t)(in && k == t) << u;
+    for (int v = 0; v < NV; ++v) {
+#pragma unroll
+      for (int s = 0; s < SPL; ++s) {
+        const uint32_t u = (uint32_t)(v * SPL + s);
+        const K k = st.sl[v].key(s);
+        km |= (uint32_t)(k == key) << u;
+        em |= (uint32_t)(k == e) << u;
+        tm |= (uint32_t)(k == t) << u;
+      }
     }
-    st.km = tile_or<L>(tile, km);
-    st.em = tile_or<L>(tile, em);
-    st.tm = tile_or<L>(tile, tm);
+    const uint32_t range = (hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & ~((1u << st.lo) - 1u);
+    st.km = km & range;
+    st.em = em & range;
+    st.tm = tm & range;
+  }
+
+  // value / retire of span bit u (register-only part selection)
+  __device__ __forceinline__ static V value(const TableRef& T, const Step& st, uint32_t u) {
+    const int part = (int)(u / SPL), s = (int)(u % SPL);
+    if constexpr (NV == 1) return Ops::template value<SPL>(T, st.base + u, st.sl[0], s);
+    V r = 0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (v == part) r = Ops::template value<SPL>(T, st.base + u, st.sl[v], s);
+    return r;
+  }
+  __device__ __forceinline__ static bool retire(const TableRef& T, const Step& st, uint32_t u) {
+    const int part = (int)(u / SPL), s = (int)(u % SPL);
+    bool won = false;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (v == part) won = Ops::template retire<SPL>(T, st.base + u, st.sl[v], s);
+    return won;
   }
 
   // in-window offset of span bit u
@@ -62,8 +95,7 @@ struct Probe {
 
   // Move past the examined part of the span.  Returns false when the
   // max_outer_attempts windows are exhausted (probing.py:214-217).
-  __device__ __forceinline__ static bool advance(const TableRef& T, Cursor& cur, const Step& st,
-                                                 uint64_t step) {
+  __device__ __forceinline__ static bool advance(const TableRef& T, Cursor& cur, const Step& st, uint64_t step) {
     cur.o += st.n_use;
     if (cur.o == WINDOW) {
       cur.attempts += WINDOW;
@@ -81,11 +113,5 @@ struct Probe {
 __device__ __forceinline__ uint32_t lowest_bit(uint32_t m) { return (uint32_t)__ffs(m) - 1; }
 // bits strictly below the lowest set bit of m (all bits when m == 0)
 __device__ __forceinline__ uint32_t below_lowest(uint32_t m) { return m ? ((m & (0u - m)) - 1u) : 0xFFFFFFFFu; }
-
-template <typename X, typename Tile>
-__device__ __forceinline__ X tile_bcast(const Tile& tile, X v, int src) {
-  if constexpr (Tile::num_threads() > 1) return tile.shfl(v, src);
-  return v;
-}
 
 }  // namespace chb

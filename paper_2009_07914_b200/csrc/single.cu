@@ -1,14 +1,18 @@
 // single.cu -- single-value COPS kernels: K0 clear, K1 insert / find_or_claim,
 // K2 retrieve, K3 erase, find (slot_of + probe stats).
 //
-// Every kernel is a persistent grid-stride loop of probe GROUPS (L lanes).  The
-// loop is flattened into one step per iteration: a group that resolves its key
-// immediately fetches the next one, so a warp never idles on the longest probe
-// of its 32 keys (memory-level parallelism is what bounds random-access work).
+// Every probe kernel is a persistent grid of CTAs that claim CHUNK-element
+// slices of the batch (sched.cuh).  Inside a chunk the probe GROUPS (L lanes)
+// run a flattened loop: one probe step per iteration, and a group that
+// resolves its key immediately takes the next one from the chunk, so no warp
+// idles on the longest probe of its keys.
 #include "dispatch.cuh"
 #include "probe.cuh"
+#include "sched.cuh"
 
 namespace chb {
+
+constexpr int CHUNK_FIND = 512;
 
 // ------------------------------------------------------------------ K0
 template <Layout LAY, typename K, typename V>
@@ -42,134 +46,142 @@ __global__ void __launch_bounds__(256) k_insert(TableRef T, const K* __restrict_
                                                 int64_t* __restrict__ slot_out) {
   using P = Probe<LAY, K, V, G>;
   using Ops = typename P::Ops;
-  auto tile = cg::tiled_partition<P::L>(cg::this_thread_block());
-  const int lane = P::L > 1 ? (int)tile.thread_rank() : 0;
-  const uint64_t ngroups = (gridDim.x * (uint64_t)blockDim.x) / P::L;
-  uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / P::L;
+  constexpr int CHUNK = chunk_for<K, V>();
+  __shared__ ChunkState cs;
+  __shared__ K s_keys[CHUNK];
+  __shared__ uint32_t s_hw[CHUNK], s_sw[CHUNK];
+  __shared__ uint8_t s_ho[CHUNK];
+  const StartSlots ss{s_hw, s_sw, s_ho};
+  __shared__ V s_vals[MODE == 0 ? CHUNK : 1];
+  __shared__ uint8_t s_status[CHUNK];
+  __shared__ int64_t s_slot[MODE == 1 ? CHUNK : 1];
+  constexpr int lane = 0;  // one thread per key (probe.cuh)
   long long occ = 0, tomb = 0, ops = 0, att = 0, win = 0;
 
-  bool active = false;
-  K key = 0;
-  V val = 0;
-  ProbeStart ps{0, 0};
-  Cursor cur;
-  cur.init(0);
-  int64_t pending = -1;
+  while (chunk_begin<CHUNK>(cs, T.work, n)) {
+    stage_keys(s_keys, ss, keys, cs, T);
+    if (MODE == 0) stage_in(s_vals, vals, cs);
+    __syncthreads();
 
-  for (;;) {
-    if (!active) {
-      while (i < n) {
-        key = ld_stream(keys + i);
-        if (key != (K)T.e && key != (K)T.t) break;
-        if (lane == 0) {  // sentinel keys: INVALID_KEY, no accounting (single_table.py:369-370)
-          status[i] = ST_INVALID;
-          if (MODE == 1) slot_out[i] = -1;
-        }
-        i += ngroups;
-      }
-      if (i >= n) break;
-      if (MODE == 0) val = ld_stream(vals + i);
-      ps = probe_start(T, key);
-      cur.init(ps.h);
-      pending = -1;
-      active = true;
-    }
-
-    typename P::Step st;
-    P::load(T, tile, cur, key, st);
-
-    int outcome = OUT_NONE;
-    uint64_t oslot = 0;
-    bool was_tomb = false;
-    bool add_chunk = true;   // final chunk accounting (false after a whole cycle)
-    uint32_t o_term = 0;
-
-    const uint32_t kb = st.km & below_lowest(st.em);
-    if (kb) {  // key present before the first empty: duplicate (single_table.py:198-200)
-      const uint32_t u = lowest_bit(kb);
-      outcome = OUT_FOUND;
-      oslot = st.base + u;
-      o_term = P::offset_of(cur, st, u);
-    } else {
-      int64_t target = -1;
-      K expected = (K)T.e;
-      if (pending < 0) {
-        const uint32_t fr = st.em | st.tm;
-        if (fr) {
-          const uint32_t u = lowest_bit(fr);
-          if (((st.tm >> u) & 1u) && st.em == 0) {
-            pending = (int64_t)(st.base + u);  // tombstone only: defer (:210-214)
-          } else {
-            target = (int64_t)(st.base + u);
-            expected = ((st.em >> u) & 1u) ? (K)T.e : (K)T.t;
+    bool active = false;
+    uint32_t li = 0;
+    K key = 0;
+    V val = 0;
+    ProbeStart ps{0, 0};
+    Cursor cur;
+    cur.init(0);
+    int64_t pending = -1;
+    for (;;) {
+      if (!active) {
+        for (;;) {
+          li = atomicAdd(&cs.next, 1u);
+          if (li >= cs.cnt) break;
+          key = s_keys[li];
+          if (key != (K)T.e && key != (K)T.t) break;
+          if (lane == 0) {  // sentinel keys: INVALID_KEY, no accounting (single_table.py:369-370)
+            s_status[li] = ST_INVALID;
+            if (MODE == 1) s_slot[li] = -1;
           }
         }
-      } else if (st.em) {
-        target = pending;  // an empty bounds the duplicate scan: claim the tombstone (:219-223)
-        expected = (K)T.t;
+        if (li >= cs.cnt) break;
+        if (MODE == 0) val = s_vals[li];
+        ps = ss.get(li);
+        cur.init(ps.h);
+        pending = -1;
+        active = true;
       }
-      bool exhausted = false;
-      if (target < 0) {
-        if (!P::advance(T, cur, st, ps.step)) {
-          exhausted = true;
-          if (pending >= 0) {  // whole cycle without an empty: claim the tombstone (:238-244)
-            target = pending;
-            expected = (K)T.t;
+
+      typename P::Step st;
+      P::load(T, cur, key, st);
+
+      int outcome = OUT_NONE;
+      uint64_t oslot = 0;
+      bool was_tomb = false;
+      bool add_chunk = true;  // final chunk accounting (false after a whole cycle)
+      uint32_t o_term = 0;
+
+      const uint32_t kb = st.km & below_lowest(st.em);
+      if (kb) {  // key present before the first empty: duplicate (single_table.py:198-200)
+        const uint32_t u = lowest_bit(kb);
+        outcome = OUT_FOUND;
+        oslot = st.base + u;
+        o_term = P::offset_of(cur, st, u);
+      } else {
+        int64_t target = -1;
+        K expected = (K)T.e;
+        if (pending < 0) {
+          const uint32_t fr = st.em | st.tm;
+          if (fr) {
+            const uint32_t u = lowest_bit(fr);
+            if (((st.tm >> u) & 1u) && st.em == 0) {
+              pending = (int64_t)(st.base + u);  // tombstone only: defer (:210-214)
+            } else {
+              target = (int64_t)(st.base + u);
+              expected = ((st.em >> u) & 1u) ? (K)T.e : (K)T.t;
+            }
+          }
+        } else if (st.em) {
+          target = pending;  // an empty bounds the duplicate scan: claim the tombstone (:219-223)
+          expected = (K)T.t;
+        }
+        bool exhausted = false;
+        if (target < 0) {
+          if (!P::advance(T, cur, st, ps.step)) {
+            exhausted = true;
+            if (pending >= 0) {  // whole cycle without an empty: claim the tombstone (:238-244)
+              target = pending;
+              expected = (K)T.t;
+            } else {
+              outcome = OUT_FULL;
+              add_chunk = false;
+            }
+          }
+        }
+        if (target >= 0) {
+          bool won = false;
+          const K seen = Ops::claim(T, (uint64_t)target, expected, key, val, MODE == 0, &won);
+          if (!exhausted) o_term = P::offset_of(cur, st, lowest_bit(st.em));
+          else add_chunk = false;
+          if (won) {
+            outcome = OUT_CLAIMED;
+            oslot = (uint64_t)target;
+            was_tomb = expected == (K)T.t;
+          } else if (seen == key) {
+            outcome = OUT_FOUND;
+            oslot = (uint64_t)target;
+          } else if (target == pending) {
+            // lost the deferred tombstone: restart the whole probe (:229-231, :244)
+            cur.attempts += add_chunk ? chunk_end(o_term, G) : 0;
+            cur.ws = ps.h;
+            cur.j = 0;
+            cur.o = 0;
+            cur.windows_seen += 1;
+            pending = -1;
           } else {
-            outcome = OUT_FULL;
-            add_chunk = false;
+            cur.attempts += G;  // lost to another key: the chunk is re-read (:232-233)
           }
         }
       }
-      if (target >= 0) {
-        // the lane holding the target slot (any lane for a deferred tombstone) does the CAS
-        const bool in_span = (uint64_t)target >= st.base && (uint64_t)target < st.base + P::A;
-        const int owner = in_span ? (int)(((uint64_t)target - st.base) / P::SPL) : 0;
-        bool won = false;
-        K seen = 0;
-        if (lane == owner) seen = Ops::claim(T, (uint64_t)target, expected, key, val, MODE == 0, &won);
-        won = tile_bcast(tile, won, owner);
-        seen = tile_bcast(tile, seen, owner);
-        if (!exhausted) o_term = P::offset_of(cur, st, lowest_bit(st.em));
-        else add_chunk = false;
-        if (won) {
-          outcome = OUT_CLAIMED;
-          oslot = (uint64_t)target;
-          was_tomb = expected == (K)T.t;
-        } else if (seen == key) {
-          outcome = OUT_FOUND;
-          oslot = (uint64_t)target;
-        } else if (target == pending) {
-          // lost the deferred tombstone: restart the whole probe (:229-231, :244)
-          cur.attempts += add_chunk ? chunk_end(o_term, G) : 0;
-          cur.ws = ps.h;
-          cur.j = 0;
-          cur.o = 0;
-          cur.windows_seen += 1;
-          pending = -1;
-        } else {
-          cur.attempts += G;  // lost to another key: the chunk is re-read (:232-233)
-        }
-      }
-    }
 
-    if (outcome != OUT_NONE) {
-      ops += 1;
-      att += (long long)(cur.attempts + (add_chunk ? chunk_end(o_term, G) : 0));
-      win += (long long)cur.windows_seen;
-      if (lane == 0) {
-        status[i] = outcome == OUT_CLAIMED ? ST_INSERTED : outcome == OUT_FOUND ? ST_DUPLICATE : ST_TABLE_FULL;
-        if (MODE == 1) slot_out[i] = outcome == OUT_FULL ? -1 : (int64_t)oslot;
+      if (outcome != OUT_NONE) {
+        ops += 1;
+        att += (long long)(cur.attempts + (add_chunk ? chunk_end(o_term, G) : 0));
+        win += (long long)cur.windows_seen;
+        if (lane == 0) {
+          s_status[li] = outcome == OUT_CLAIMED ? ST_INSERTED : outcome == OUT_FOUND ? ST_DUPLICATE : ST_TABLE_FULL;
+          if (MODE == 1) s_slot[li] = outcome == OUT_FULL ? -1 : (int64_t)oslot;
+        }
+        if (outcome == OUT_CLAIMED) {
+          occ += 1;
+          if (was_tomb) tomb -= 1;
+        }
+        active = false;
       }
-      if (outcome == OUT_CLAIMED) {
-        occ += 1;
-        if (was_tomb) tomb -= 1;
-      }
-      active = false;
-      i += ngroups;
     }
+    __syncthreads();
+    stage_out(status, s_status, cs);
+    if (MODE == 1) stage_out(slot_out, s_slot, cs);
   }
-  if (P::L > 1 && lane != 0) occ = tomb = ops = att = win = 0;
   const long long v[5] = {ops, att, win, occ, tomb};
   long long* const dst[5] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts,
                              (long long*)&T.ctr->windows, &T.ctr->occupied, &T.ctr->tombstones};
@@ -178,7 +190,7 @@ __global__ void __launch_bounds__(256) k_insert(TableRef T, const K* __restrict_
 
 // ------------------------------------------------------------------ K2
 // MODE 0: retrieve_bulk (single_table.py:376-408): value + found flag
-// MODE 1: find (slot_of / retrieve_with_stats, :317-336): slot, attempts, windows
+// MODE 1: find (slot_of / retrieve_with_stats, :317-336): slot, attempts, windows, value
 // MODE 2: erase (:338-351): retire the key (layout.py:224-243)
 template <Layout LAY, typename K, typename V, int G, int MODE>
 __global__ void __launch_bounds__(256) k_lookup(TableRef T, const K* __restrict__ keys, uint64_t n,
@@ -188,95 +200,99 @@ __global__ void __launch_bounds__(256) k_lookup(TableRef T, const K* __restrict_
                                                 uint32_t* __restrict__ win_out) {
   using P = Probe<LAY, K, V, G>;
   using Ops = typename P::Ops;
-  auto tile = cg::tiled_partition<P::L>(cg::this_thread_block());
-  const int lane = P::L > 1 ? (int)tile.thread_rank() : 0;
-  const uint64_t ngroups = (gridDim.x * (uint64_t)blockDim.x) / P::L;
-  uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / P::L;
+  constexpr int CH = MODE == 1 ? CHUNK_FIND : chunk_for<K, V>();
+  __shared__ ChunkState cs;
+  __shared__ K s_keys[CH];
+  __shared__ uint32_t s_hw[CH], s_sw[CH];
+  __shared__ uint8_t s_ho[CH];
+  const StartSlots ss{s_hw, s_sw, s_ho};
+  __shared__ V s_vals[MODE == 2 ? 1 : CH];
+  __shared__ uint8_t s_flag[MODE == 1 ? 1 : CH];
+  __shared__ int64_t s_slot[MODE == 1 ? CH : 1];
+  __shared__ uint32_t s_att[MODE == 1 ? CH : 1];
+  __shared__ uint32_t s_win[MODE == 1 ? CH : 1];
+  constexpr int lane = 0;  // one thread per key (probe.cuh)
   long long ops = 0, att = 0, win = 0, occ = 0, tomb = 0;
 
-  bool active = false;
-  K key = 0;
-  ProbeStart ps{0, 0};
-  Cursor cur;
-  cur.init(0);
-
-  for (;;) {
-    if (!active) {
-      while (i < n) {
-        key = ld_stream(keys + i);
-        if (key != (K)T.e && key != (K)T.t) break;
-        if (MODE == 0) ops += lane == 0;  // retrieve_bulk counts every query (:403)
-        if (lane == 0) {
-          if (MODE == 0) { st_stream(vals_out + i, (V)0); st_stream(flag + i, (uint8_t)0); }
-          if (MODE == 1) {
-            slot_out[i] = -1;
-            if (vals_out) vals_out[i] = 0;
-            if (att_out) att_out[i] = 0;
-            if (win_out) win_out[i] = 0;
+  while (chunk_begin<CH>(cs, T.work, n)) {
+    stage_keys(s_keys, ss, keys, cs, T);
+    __syncthreads();
+    bool active = false;
+    uint32_t li = 0;
+    K key = 0;
+    ProbeStart ps{0, 0};
+    Cursor cur;
+    cur.init(0);
+    for (;;) {
+      if (!active) {
+        for (;;) {
+          li = atomicAdd(&cs.next, 1u);
+          if (li >= cs.cnt) break;
+          key = s_keys[li];
+          if (key != (K)T.e && key != (K)T.t) break;
+          if (MODE == 0) ops += lane == 0;  // retrieve_bulk counts every query (:403)
+          if (lane == 0) {
+            if (MODE == 0) { s_vals[li] = 0; s_flag[li] = 0; }
+            if (MODE == 1) { s_slot[li] = -1; s_att[li] = 0; s_win[li] = 0; s_vals[li] = 0; }
+            if (MODE == 2) s_flag[li] = 0;
           }
-          if (MODE == 2) flag[i] = 0;
         }
-        i += ngroups;
+        if (li >= cs.cnt) break;
+        ps = ss.get(li);
+        cur.init(ps.h);
+        active = true;
       }
-      if (i >= n) break;
-      ps = probe_start(T, key);
-      cur.init(ps.h);
-      active = true;
-    }
 
-    typename P::Step st;
-    P::load(T, tile, cur, key, st);
-    const uint32_t kb = st.km & below_lowest(st.em);
-    bool done = false, found = false;
-    uint32_t u = 0;
-    uint64_t attempts = 0;
-    if (kb) {
-      u = lowest_bit(kb);
-      found = done = true;
-      attempts = cur.attempts + chunk_end(P::offset_of(cur, st, u), G);
-    } else if (st.em) {
-      done = true;
-      attempts = cur.attempts + chunk_end(P::offset_of(cur, st, lowest_bit(st.em)), G);
-    } else if (!P::advance(T, cur, st, ps.step)) {
-      done = true;
-      attempts = cur.attempts;
-    }
-    if (!done) continue;
+      typename P::Step st;
+      P::load(T, cur, key, st);
+      const uint32_t kb = st.km & below_lowest(st.em);
+      bool done = false, found = false;
+      uint32_t u = 0;
+      uint64_t attempts = 0;
+      if (kb) {
+        u = lowest_bit(kb);
+        found = done = true;
+        attempts = cur.attempts + chunk_end(P::offset_of(cur, st, u), G);
+      } else if (st.em) {
+        done = true;
+        attempts = cur.attempts + chunk_end(P::offset_of(cur, st, lowest_bit(st.em)), G);
+      } else if (!P::advance(T, cur, st, ps.step)) {
+        done = true;
+        attempts = cur.attempts;
+      }
+      if (!done) continue;
 
-    const int owner = (int)(u / P::SPL);
-    const int s = (int)(u % P::SPL);
+      if (MODE == 0 || MODE == 1) {
+        s_vals[li] = found ? P::value(T, st, u) : (V)0;
+        if (MODE == 0) s_flag[li] = (uint8_t)found;
+        if (MODE == 1 && lane == 0) {
+          s_slot[li] = found ? (int64_t)(st.base + u) : -1;
+          s_att[li] = (uint32_t)attempts;
+          s_win[li] = (uint32_t)cur.windows_seen;
+        }
+      } else {
+        const bool won = found && P::retire(T, st, u);
+        s_flag[li] = won;
+        if (won) { occ -= 1; tomb += 1; }
+      }
+      ops += 1;
+      att += (long long)attempts;
+      win += (long long)cur.windows_seen;
+      active = false;
+    }
+    __syncthreads();
     if (MODE == 0) {
-      V v = 0;
-      if (found && lane == owner) v = Ops::template value<P::SPL>(T, st.base + u, st.sl, s);
-      if (lane == owner) {
-        st_stream(vals_out + i, found ? v : (V)0);
-        st_stream(flag + i, (uint8_t)found);
-      }
+      stage_out(vals_out, s_vals, cs);
+      stage_out(flag, s_flag, cs);
     } else if (MODE == 1) {
-      if (vals_out) {
-        V v = 0;
-        if (found && lane == owner) v = Ops::template value<P::SPL>(T, st.base + u, st.sl, s);
-        if (lane == owner) vals_out[i] = v;
-      }
-      if (lane == 0) {
-        slot_out[i] = found ? (int64_t)(st.base + u) : -1;
-        if (att_out) att_out[i] = (uint32_t)attempts;
-        if (win_out) win_out[i] = (uint32_t)cur.windows_seen;
-      }
+      stage_out(slot_out, s_slot, cs);
+      if (att_out) stage_out(att_out, s_att, cs);
+      if (win_out) stage_out(win_out, s_win, cs);
+      if (vals_out) stage_out(vals_out, s_vals, cs);
     } else {
-      bool won = false;
-      if (found && lane == owner) won = Ops::template retire<P::SPL>(T, st.base + u, st.sl, s);
-      won = tile_bcast(tile, won, owner);
-      if (lane == 0) flag[i] = won;
-      if (won) { occ -= 1; tomb += 1; }
+      stage_out(flag, s_flag, cs);
     }
-    ops += 1;
-    att += (long long)attempts;
-    win += (long long)cur.windows_seen;
-    active = false;
-    i += ngroups;
   }
-  if (P::L > 1 && lane != 0) ops = att = win = occ = tomb = 0;
   const long long v[5] = {ops, att, win, occ, tomb};
   long long* const dst[5] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts,
                              (long long*)&T.ctr->windows, &T.ctr->occupied, &T.ctr->tombstones};
@@ -294,31 +310,29 @@ struct SingleKernels {
   }
   static int insert(const Launch& lc, const TableRef& T, const void* keys, const void* vals, uint64_t n,
                     uint8_t* status, int64_t* slot_out, int mode) {
-    using P = Probe<LAY, K, V, G>;
     if (mode == 0) {
       auto kern = k_insert<LAY, K, V, G, 0>;
-      return launch_persistent(lc, (const void*)kern, n, P::L, [&](dim3 g, dim3 b) {
+      return launch_chunked(lc, T, (const void*)kern, n, chunk_for<K, V>(), [&](dim3 g, dim3 b) {
         kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status, slot_out);
       });
     }
     auto kern = k_insert<LAY, K, V, G, 1>;
-    return launch_persistent(lc, (const void*)kern, n, P::L, [&](dim3 g, dim3 b) {
+    return launch_chunked(lc, T, (const void*)kern, n, chunk_for<K, V>(), [&](dim3 g, dim3 b) {
       kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status, slot_out);
     });
   }
   static int lookup(const Launch& lc, const TableRef& T, const void* keys, uint64_t n, void* vals_out,
                     uint8_t* flag, int64_t* slot_out, uint32_t* att_out, uint32_t* win_out, int mode) {
-    using P = Probe<LAY, K, V, G>;
-#define CHB_LOOKUP(M)                                                                                  \
+#define CHB_LOOKUP(M, CH)                                                                              \
   {                                                                                                    \
     auto kern = k_lookup<LAY, K, V, G, M>;                                                             \
-    return launch_persistent(lc, (const void*)kern, n, P::L, [&](dim3 g, dim3 b) {                     \
+    return launch_chunked(lc, T, (const void*)kern, n, CH, [&](dim3 g, dim3 b) {                       \
       kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, (V*)vals_out, flag, slot_out, att_out, win_out); \
     });                                                                                                \
   }
-    if (mode == 0) CHB_LOOKUP(0)
-    if (mode == 1) CHB_LOOKUP(1)
-    CHB_LOOKUP(2)
+    if (mode == 0) CHB_LOOKUP(0, (chunk_for<K, V>()))
+    if (mode == 1) CHB_LOOKUP(1, CHUNK_FIND)
+    CHB_LOOKUP(2, (chunk_for<K, V>()))
 #undef CHB_LOOKUP
   }
 };

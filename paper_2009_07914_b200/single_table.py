@@ -112,6 +112,11 @@ class _TableBase:
         _lib.check(_lib.lib().ch_reset_probe_counters(self._dt.handle, self._stream()),
                    "reset_probe_counters")
 
+    def set_locality(self, mode) -> None:
+        """Region-ordered execution of big batches: "auto" (default), "off" or "on"."""
+        code = {"auto": 0, "off": 1, "on": 2}.get(mode, mode)
+        _lib.check(_lib.lib().ch_set_locality(self._dt.handle, int(code)), "set_locality")
+
     def synchronize(self) -> None:
         _lib.check(_lib.lib().ch_synchronize(self._dt.handle), "synchronize")
 

@@ -66,10 +66,12 @@ def test_sequential_replay_is_slot_exact(idx):
 
 # ------------------------------------------------ bulk replay: semantic parity
 
+@pytest.mark.parametrize("loc", ["off", "on"])
 @pytest.mark.parametrize("idx", range(11))
-def test_bulk_replay_semantics(idx):
+def test_bulk_replay_semantics(idx, loc):
     sc = load("single.json")["scenarios"][idx]
     t = table_from(sc)
+    t.set_locality(loc)
     model: dict[int, int] = {}
     any_full = False
     for step in sc["steps"]:
@@ -117,16 +119,17 @@ def test_bulk_replay_semantics(idx):
     ("soa", 64, 64, 4), ("soa", 32, 64, 8), ("soa", 64, 32, 16), ("soa", 32, 32, 32),
     ("aos", 64, 64, 8), ("aos", 32, 32, 4), ("aos", 32, 64, 2), ("aos", 64, 32, 1),
 ])
-@pytest.mark.parametrize("rho", [0.8, 0.95])
-def test_bulk_unique_vs_oracle(layout, kb, vb, g, rho):
+@pytest.mark.parametrize("rho,loc", [(0.8, "auto"), (0.95, "auto"), (0.95, "on")])
+def test_bulk_unique_vs_oracle(layout, kb, vb, g, rho, loc):
     n = 1 << 18
-    rng = np.random.default_rng(zlib.crc32(f"{layout}{kb}{vb}{g}{rho}".encode()))
+    rng = np.random.default_rng(zlib.crc32(f"{layout}{kb}{vb}{g}{rho}{loc}".encode()))
     hi = (1 << kb) - 3
     keys = rng.permutation(np.unique(rng.integers(1, hi, size=3 * n, dtype=np.uint64)))
     present, absent = keys[:n], keys[n:2 * n]
     vals = rng.integers(0, (1 << vb) - 1, size=n, dtype=np.uint64)
     cap = int(np.ceil(n / rho))
     t = SingleValueHashTable(cap, layout=layout, key_bits=kb, value_bits=vb, group_width=g)
+    t.set_locality(loc)
     st = t.insert_device(present, vals).cpu().numpy()
     assert (st == 0).all()
     assert t.occupied == n
@@ -301,8 +304,10 @@ def test_in_batch_duplicates():              # :190-197
     assert t.retrieve(5) in (1, 3, 4) and t.retrieve(6) in (2, 5)
 
 
-def test_same_key_storm_single_winner():     # :278-298 (8 threads -> 1M lanes)
+@pytest.mark.parametrize("loc", ["off", "on"])
+def test_same_key_storm_single_winner(loc):  # :278-298 (8 threads -> 1M lanes)
     t = SingleValueHashTable(256, layout="packed", key_bits=32, value_bits=32)
+    t.set_locality(loc)
     n = 1 << 20
     keys = torch.full((n,), 777, dtype=torch.int32, device="cuda")
     vals = torch.arange(n, dtype=torch.int32, device="cuda")
@@ -365,3 +370,27 @@ def test_find_or_claim():
     assert st == INSERTED and slot == t.slot_of(42)
     st2, slot2 = t.find_or_claim(42)
     assert st2 == DUP and slot2 == slot
+
+
+def test_locality_path_at_scale_matches_direct():
+    """2^24 keys in a 128 MiB+ table: region-ordered and direct execution agree bit for bit."""
+    n = 1 << 24
+    rng = np.random.default_rng(11)
+    keys = torch.from_numpy(rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=n + n // 4,
+                                                                   dtype=np.uint64)))[:n].astype(np.uint32)
+                            .view(np.int32)).cuda()
+    vals = torch.arange(n, dtype=torch.int32, device="cuda")
+    out = []
+    for loc in ("off", "on"):
+        t = SingleValueHashTable(int(n / 0.95), layout="packed", key_bits=32, value_bits=32, group_width=8)
+        t.set_locality(loc)
+        st = t.insert_device(keys, vals)
+        assert (st == 0).all().item() and t.occupied == n
+        dup = keys[: n // 2]
+        st2 = t.insert_device(dup, vals[: n // 2])
+        assert (st2 == 1).all().item()
+        v, f = t.retrieve_device(keys)
+        assert f.bool().all().item() and (v == vals).all().item()
+        miss = keys[: 1 << 20] ^ 0x5A5A5A5A
+        out.append(t.retrieve_device(miss))
+    assert torch.equal(out[0][1], out[1][1]) and torch.equal(out[0][0], out[1][0])

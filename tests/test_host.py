@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_library_exports_every_declared_symbol():
     header = open(os.path.join(ROOT, "include", "coophash_b200.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(ch_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|uint64_t|const char\*)\s+(ch_\w+)\s*\(", header, re.M))
     assert declared, "no declarations parsed"
     lib = _lib.lib()  # loads without a GPU
     for name in declared:
