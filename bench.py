@@ -220,6 +220,8 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", default="", help="write a g x load sweep to this JSON file")
+    ap.add_argument("--locality", default="auto", choices=("auto", "on", "off"),
+                    help="region-ordered execution of the batch (csrc/locality.cu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     if args.impl == "reference":
@@ -244,6 +246,7 @@ def main() -> None:
     cap = math.ceil(n * (1.001 if world > 1 else 1.0) / args.load)
     table = SingleValueHashTable(cap, layout="packed", key_bits=32, value_bits=32,
                                  group_width=args.group_width, device=local)
+    table.set_locality(args.locality)
     front = ShardedTable(table) if world > 1 else table
     stream = torch.cuda.current_stream(dev)
     status = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -281,6 +284,8 @@ def main() -> None:
     barrier()
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    table.kernel_times()
+    table.kernel_timing(True)
     launches0 = _lib.lib().ch_kernel_launches()
     with ClockSampler(local) as clocks:
         barrier()
@@ -292,6 +297,10 @@ def main() -> None:
         t_end.record(stream)
         barrier()
     launches = _lib.lib().ch_kernel_launches() - launches0
+    table.kernel_timing(False)
+    ktimes = table.kernel_times()  # probe kernels in launch order: [insert, lookup] per step
+    k_ins_ms = statistics.mean(ktimes[0::2]) if len(ktimes) >= 2 else float("nan")
+    k_ret_ms = statistics.mean(ktimes[1::2]) if len(ktimes) >= 2 else float("nan")
     total_ms = t_start.elapsed_time(t_end)
     clear_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     ins_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
@@ -357,13 +366,16 @@ def main() -> None:
         peak, peak_kind = measured_peak()
         ins_gops = n * world / (ins_ms_max * 1e-3) / 1e9
         ret_gops = n * world / (ret_ms_max * 1e-3) / 1e9
-        # dominant kernel: the longer of insert / retrieve (single GPU: one launch each)
-        if ins_ms >= ret_ms:
-            kname, kms, kbytes = "k_insert", ins_ms, INSERT_BYTES
+        # dominant kernel: the longer of the insert / retrieve probe kernels, timed with
+        # CUDA events inside the library on the stream they run on (one launch each per step)
+        if k_ins_ms >= k_ret_ms:
+            kname, kms, kbytes = "k_insert", k_ins_ms, INSERT_BYTES
         else:
-            kname, kms, kbytes = "k_lookup(retrieve)", ret_ms, RETRIEVE_BYTES
-        achieved = kbytes * n / (kms * 1e-3) / 1e9
-        traffic = ncu_traffic().get(kname.split("(")[0] if world == 1 else "", None)
+            kname, kms, kbytes = "k_lookup", k_ret_ms, RETRIEVE_BYTES
+        keys_per_launch = n if world == 1 else n  # weak scaling: ~n keys per rank and launch
+        achieved = kbytes * keys_per_launch / (kms * 1e-3) / 1e9
+        tr = ncu_traffic().get(kname) if world == 1 else None
+        traffic = tr.get("dram_bytes") if isinstance(tr, dict) else tr
         cpu = None
         if world == 1 and not args.no_cpu:
             threads = os.cpu_count() or 1
@@ -378,27 +390,30 @@ def main() -> None:
             "config": {"workload": "SingleValueHashTable packed 32|32 (BASELINE configs[1])" if world == 1 else
                        "ShardedTable packed 32|32, hash-partitioned, NCCL all_to_all (BASELINE configs[4])",
                        "keys_per_gpu": n, "load": args.load, "capacity_per_gpu": table.capacity,
-                       "group_width": args.group_width, "parallelism": f"hash-partitioned x{world}",
+                       "group_width": args.group_width, "locality": args.locality,
+                       "parallelism": f"hash-partitioned x{world}",
                        "l2": "inputs (2 GiB) and table (2.1 GiB) exceed the 126 MB L2; no flush"},
             "insert_gops": ins_gops, "retrieve_gops": ret_gops,
-            "phase_ms": {"clear": clear_ms, "insert": ins_ms, "retrieve": ret_ms},
+            "phase_ms": {"clear": clear_ms, "insert": ins_ms, "retrieve": ret_ms,
+                         "k_insert": k_ins_ms, "k_lookup": k_ret_ms},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "bytes_per_op": kbytes, "traffic": traffic},
+                         "bytes_per_op": kbytes, "ops_per_launch": keys_per_launch, "traffic": traffic,
+                         "kernel_ms": kms},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks.summary(),
             "verified": ok,
         }
         print(json.dumps(line), flush=True)
 
     if args.sweep and world == 1:
-        sweep(args.sweep, n, dev)
+        sweep(args.sweep, n, dev, args.locality)
     if world > 1:
         dist.destroy_process_group()
     if not ok:
         sys.exit(2)
 
 
-def sweep(path: str, n: int, dev) -> None:
+def sweep(path: str, n: int, dev, locality: str = "auto") -> None:
     """g x load sweep of the single-GPU insert / retrieve rates (BASELINE configs[1])."""
     import torch
     from paper_2009_07914_b200 import SingleValueHashTable, _lib
@@ -409,6 +424,7 @@ def sweep(path: str, n: int, dev) -> None:
         for g in (1, 2, 4, 8, 16, 32):
             t = SingleValueHashTable(math.ceil(n / load), layout="packed", key_bits=32, value_bits=32,
                                      group_width=g, device=dev.index)
+            t.set_locality(locality)
             st = torch.empty(n, dtype=torch.uint8, device=dev)
             ov = torch.empty(n, dtype=torch.int32, device=dev)
             of = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -426,7 +442,7 @@ def sweep(path: str, n: int, dev) -> None:
                     ins.append(e[0].elapsed_time(e[1]))
                     ret.append(e[1].elapsed_time(e[2]))
             c = t.probe_counters()
-            rows.append({"load": load, "group_width": g, "insert_ms": statistics.mean(ins),
+            rows.append({"load": load, "group_width": g, "locality": locality, "insert_ms": statistics.mean(ins),
                          "retrieve_ms": statistics.mean(ret), "insert_gops": n / statistics.mean(ins) / 1e6,
                          "retrieve_gops": n / statistics.mean(ret) / 1e6,
                          "mean_attempts": c.attempts / max(1, c.ops)})

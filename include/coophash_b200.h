@@ -89,6 +89,11 @@ int ch_synchronize(ch_table* t);
 /* region-ordered execution of big batches (csrc/locality.cu): 0 auto (table > 256 MiB and
  * n >= c/16), 1 never, 2 always.  Results are identical; only the schedule changes. */
 int ch_set_locality(ch_table* t, int mode);
+/* CUDA-event timing of the table's probe kernels (insert / lookup / multi passes):
+ * enable, then read each launch's device time in launch order (up to cap entries) and
+ * the number of launches timed (synchronizes, resets) */
+int ch_kernel_timing(ch_table* t, int enable);
+int ch_kernel_time(ch_table* t, double* ms, uint64_t cap, uint64_t* launches);
 
 /* ---- single-value (and bucket key store) ---- */
 /* insert_bulk (single_table.py:355-374): d_status[n] */

@@ -78,6 +78,8 @@ struct ch_table {
   std::mutex mu;
   int sms = 148;
   int loc_mode = 0;  // 0 auto, 1 never, 2 always (region-ordered execution, locality.cu)
+  bool timing = false;
+  KernelTimer timer;
 };
 
 namespace {
@@ -112,6 +114,7 @@ struct Ordered {
     lc.stream = s;
     lc.device = t->cfg.device;
     lc.sms = t->sms;
+    lc.timer = t->timing ? &t->timer : nullptr;
     cudaStreamWaitEvent(s, t->last, 0);
   }
   int done(int rc) {
@@ -393,6 +396,32 @@ int ch_clear(ch_table* t, void* stream) {
   }
   t->host_ops = 0;
   return o.done(rc);
+}
+
+int ch_kernel_timing(ch_table* t, int enable) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  std::lock_guard<std::mutex> lock(t->mu);
+  t->timing = enable != 0;
+  return CH_OK;
+}
+
+int ch_kernel_time(ch_table* t, double* ms, uint64_t cap, uint64_t* launches) {
+  if (!t || !launches) return fail(CH_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard dev(t->cfg.device);
+  int rc = check(cudaEventSynchronize(t->last), "synchronize");
+  uint64_t i = 0;
+  for (auto& p : t->timer.ev) {
+    float x = 0;
+    if (!rc && cudaEventElapsedTime(&x, p.first, p.second) != cudaSuccess) x = -1;
+    if (ms && i < cap) ms[i] = x;
+    ++i;
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  *launches = t->timer.ev.size();
+  t->timer.ev.clear();
+  return rc;
 }
 
 int ch_set_locality(ch_table* t, int mode) {

@@ -7,15 +7,23 @@
 #include <string>
 #include <unordered_map>
 #include <utility>
+#include <vector>
 
 #include "common.cuh"
 
 namespace chb {
 
+// Optional CUDA-event timing of the probe kernels (bench.py: the dominant
+// kernel's own duration, on the stream it runs on).
+struct KernelTimer {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+};
+
 struct Launch {
   cudaStream_t stream;
   int device;
   int sms;
+  KernelTimer* timer = nullptr;
 };
 
 struct TypeSel {
@@ -75,8 +83,15 @@ int launch_chunked(const Launch& lc, const TableRef& T, const void* kern, uint64
   const uint64_t want = (items + chunk - 1) / chunk;
   const uint64_t full = (uint64_t)lc.sms * (uint64_t)occupancy(kern, threads);
   const uint64_t blocks = want < full ? want : full;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (lc.timer && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess)
+    cudaEventRecord(e0, lc.stream);
   fn(dim3((unsigned)blocks), dim3(threads));
   count_launch();
+  if (e1) {
+    cudaEventRecord(e1, lc.stream);
+    lc.timer->ev.emplace_back(e0, e1);
+  }
   return cuda_check(cudaGetLastError(), "kernel launch");
 }
 

@@ -117,6 +117,18 @@ class _TableBase:
         code = {"auto": 0, "off": 1, "on": 2}.get(mode, mode)
         _lib.check(_lib.lib().ch_set_locality(self._dt.handle, int(code)), "set_locality")
 
+    def kernel_timing(self, enable: bool = True) -> None:
+        """Record CUDA events around every probe-kernel launch of this table."""
+        _lib.check(_lib.lib().ch_kernel_timing(self._dt.handle, int(bool(enable))), "kernel_timing")
+
+    def kernel_times(self) -> list[float]:
+        """Device time (ms) of each timed probe-kernel launch, in launch order; resets."""
+        import ctypes as C
+        cnt = C.c_uint64(0)
+        buf = (C.c_double * 4096)()
+        _lib.check(_lib.lib().ch_kernel_time(self._dt.handle, buf, 4096, C.byref(cnt)), "kernel_time")
+        return [buf[i] for i in range(min(cnt.value, 4096))]
+
     def synchronize(self) -> None:
         _lib.check(_lib.lib().ch_synchronize(self._dt.handle), "synchronize")
 
