@@ -325,21 +325,20 @@ def main() -> None:
         hv = vals.cpu().pin_memory()
         host_v = torch.empty(n, dtype=torch.int32).pin_memory()
         host_f = torch.empty(n, dtype=torch.uint8).pin_memory()
+        host_s = torch.empty(n, dtype=torch.uint8).pin_memory()
 
         def e2e_step():
             _lib.check(_lib.lib().ch_clear(table._dt.handle, stream.cuda_stream), "clear")
-            dk = hk.to(dev, non_blocking=True)
-            dv = hv.to(dev, non_blocking=True)
             if world > 1:
+                dk = hk.to(dev, non_blocking=True)
+                dv = hv.to(dev, non_blocking=True)
                 front.insert_device(dk, dv)
-                dk2 = hk.to(dev, non_blocking=True)
-                v2, f2 = front.retrieve_device(dk2)
-            else:
-                table.insert_device(dk, dv, status=status)
-                dk2 = hk.to(dev, non_blocking=True)
-                v2, f2 = table.retrieve_device(dk2, values_out=out_v, found_out=out_f)
-            host_v.copy_(v2, non_blocking=True)
-            host_f.copy_(f2, non_blocking=True)
+                v2, f2 = front.retrieve_device(hk.to(dev, non_blocking=True))
+                host_v.copy_(v2, non_blocking=True)
+                host_f.copy_(f2, non_blocking=True)
+                return host_v, host_f
+            table.insert_host(hk, hv, status_out=host_s)  # public API: pinned host buffers in and out
+            return table.retrieve_host(hk, values_out=host_v, found_out=host_f)
 
         for _ in range(2):
             e2e_step()
@@ -348,19 +347,19 @@ def main() -> None:
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            e2e_step()
+            res_v, res_f = e2e_step()
         e1.record(stream)
         barrier()
         e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-        e2e_ok = bool((host_v == hv).all().item() and (host_f == 1).all().item())
+        e2e_ok = bool((res_v == hv).all().item() and (res_f == 1).all().item())
         ok = ok and e2e_ok
         e2e = {"value": 2 * n * world / (e2e_ms.item() * 1e-3) / 1e9, "unit": "G ops/s",
-               "h2d_bytes_per_step": 3 * 4 * n, "d2h_bytes_per_step": 5 * n,
+               "h2d_bytes_per_step": 3 * 4 * n, "d2h_bytes_per_step": 6 * n,
                "ms_per_step": e2e_ms.item(),
-               "path": "pinned host keys/values -> insert_device; pinned host keys -> retrieve_device -> "
-                       "pinned host values/found (one CUDA stream)"}
+               "path": "pinned host keys/values -> insert_host; pinned host keys -> retrieve_host -> "
+                       "pinned host values/found (chunked, H2D / kernels / D2H overlapped on 3 streams)"}
 
     if rank == 0:
         peak, peak_kind = measured_peak()

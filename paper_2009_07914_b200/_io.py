@@ -75,3 +75,49 @@ def stream_of(device: int, stream=None) -> int:
 def split_pairs(pairs) -> tuple[list, list]:
     pairs = list(pairs)
     return [k for k, _ in pairs], [v for _, v in pairs]
+
+
+def pipelined(device: int, inputs: list, outputs: list, run, chunk: int) -> None:
+    """Stream host inputs through a device op in chunks: H2D copies, kernels and D2H
+    copies of consecutive chunks overlap on three CUDA streams.
+
+    inputs / outputs: equal-length pinned host tensors (outputs are filled in place).
+    run(list_of_device_input_slices, stream) -> list of device outputs, one per output.
+    The caller's current stream waits for the whole pipeline before returning.
+    """
+    n = inputs[0].numel()
+    if n == 0:
+        return
+    dev = torch.device("cuda", device)
+    compute = torch.cuda.current_stream(dev)
+    s_in = torch.cuda.Stream(dev)
+    s_out = torch.cuda.Stream(dev)
+    nb = 2
+    bufs = [[torch.empty(min(chunk, n), dtype=x.dtype, device=dev) for x in inputs] for _ in range(nb)]
+    free = [torch.cuda.Event() for _ in range(nb)]
+    s_in.wait_stream(compute)
+    for c, lo in enumerate(range(0, n, chunk)):
+        hi = min(n, lo + chunk)
+        m = hi - lo
+        b = c % nb
+        ev_in = torch.cuda.Event()
+        with torch.cuda.stream(s_in):
+            if c >= nb:
+                s_in.wait_event(free[b])
+            for d, x in zip(bufs[b], inputs):
+                d[:m].copy_(x[lo:hi], non_blocking=True)
+            ev_in.record(s_in)
+        compute.wait_event(ev_in)
+        outs = run([d[:m] for d in bufs[b]], compute)
+        ev_done = torch.cuda.Event()
+        ev_done.record(compute)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_done)
+            for o, y in zip(outs, outputs):
+                o.record_stream(s_out)
+                y[lo:hi].copy_(o, non_blocking=True)
+            free[b].record(s_out)
+    compute.wait_stream(s_out)
+    for bb in bufs:
+        for d in bb:
+            d.record_stream(s_in)

@@ -59,6 +59,17 @@ def statuses_from_codes(codes: np.ndarray) -> list[InsertStatus]:
     return [STATUS_BY_CODE[c] for c in codes.tolist()]
 
 
+def _host_tensor(x, bits: int) -> torch.Tensor:
+    """Host data as a pinned integer tensor of the storage width."""
+    dt = _io.torch_dtype(bits)
+    if isinstance(x, torch.Tensor) and not x.is_cuda and x.dtype == dt:
+        return x if x.is_pinned() else x.pin_memory()
+    if isinstance(x, torch.Tensor):
+        x = x.cpu().numpy()
+    arr = _io.to_numpy(x, bits)
+    return torch.from_numpy(arr.view(np.int32 if bits <= 32 else np.int64)).pin_memory()
+
+
 class _TableBase:
     """Construction and gauges shared by the three table kinds."""
 
@@ -217,6 +228,38 @@ class SingleValueHashTable(_TableBase):
                                       vals.data_ptr() if vals is not None else None,
                                       self._stream(stream)), "find")
         return slots, att, win, vals
+
+    # -- host-buffer bulk API (pipelined H2D / kernels / D2H) ---------------------
+    def insert_host(self, keys, values, chunk: int | None = None,
+                    status_out: torch.Tensor | None = None) -> torch.Tensor:
+        """Bulk insert from (pinned) host tensors; returns pinned host status codes.
+        Copies and kernels of consecutive chunks overlap (_io.pipelined); returns
+        once the statuses are on the host."""
+        keys = _host_tensor(keys, self.key_bits)
+        values = _host_tensor(values, self.value_bits)
+        status = status_out if status_out is not None else \
+            torch.empty(keys.numel(), dtype=torch.uint8, pin_memory=True)
+        _io.pipelined(self.device, [keys, values], [status],
+                      lambda d, s: [self.insert_device(d[0], d[1], stream=s)], chunk or self._host_chunk())
+        torch.cuda.current_stream(self.device).synchronize()
+        return status
+
+    def retrieve_host(self, keys, chunk: int | None = None, values_out: torch.Tensor | None = None,
+                      found_out: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+        """Bulk retrieve for (pinned) host keys; returns pinned host (values, found)."""
+        keys = _host_tensor(keys, self.key_bits)
+        n = keys.numel()
+        vals = values_out if values_out is not None else \
+            torch.empty(n, dtype=_io.torch_dtype(self.value_bits), pin_memory=True)
+        found = found_out if found_out is not None else torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        _io.pipelined(self.device, [keys], [vals, found],
+                      lambda d, s: list(self.retrieve_device(d[0], stream=s)), chunk or self._host_chunk())
+        torch.cuda.current_stream(self.device).synchronize()
+        return vals, found
+
+    def _host_chunk(self) -> int:
+        # big enough to keep region-ordered execution on (n >= c/16), small enough to overlap
+        return max(1 << 20, -(-self.capacity // 12))
 
     # -- element operations (single_table.py:273-351) ---------------------------
     def insert(self, key: int, value: int) -> InsertStatus:

@@ -394,3 +394,22 @@ def test_locality_path_at_scale_matches_direct():
         miss = keys[: 1 << 20] ^ 0x5A5A5A5A
         out.append(t.retrieve_device(miss))
     assert torch.equal(out[0][1], out[1][1]) and torch.equal(out[0][0], out[1][0])
+
+
+def test_host_pipeline_matches_device_path():
+    """insert_host / retrieve_host (chunked H2D / kernel / D2H overlap) == the device API."""
+    n = (1 << 22) + 12345
+    rng = np.random.default_rng(21)
+    keys = rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=n + n // 4, dtype=np.uint64)))[:n]
+    vals = rng.integers(0, 1 << 32, size=n, dtype=np.uint64)
+    t = SingleValueHashTable(int(n / 0.9), layout="packed", key_bits=32, value_bits=32, group_width=8)
+    st = t.insert_host(keys, vals, chunk=1 << 20)
+    assert (st.numpy() == 0).all() and t.occupied == n
+    st2 = t.insert_host(keys[:1000], vals[:1000], chunk=300)
+    assert (st2.numpy() == 1).all()
+    v, f = t.retrieve_host(np.concatenate([keys, keys[:10] ^ np.uint64(0xFFFF)]), chunk=1 << 19)
+    v = v.numpy().view(np.uint32)
+    f = f.numpy()
+    assert f[:n].all() and (v[:n] == vals.astype(np.uint32)).all()
+    dv, df = t.retrieve_device(keys[:4096])
+    assert (dv.cpu().numpy().view(np.uint32) == v[:4096]).all()
