@@ -39,6 +39,10 @@ __global__ void __launch_bounds__(256) k_clear(TableRef T, int zero_values) {
 //         slot written to slot_out (the bucket list's key store).
 enum Outcome : int { OUT_NONE = -1, OUT_CLAIMED = 0, OUT_FOUND = 1, OUT_FULL = 2 };
 
+// find_or_claim also stages an int64 slot per element
+template <typename K, typename V, int MODE>
+constexpr int insert_chunk() { return MODE == 1 ? 1024 : chunk_for<K, V>(); }
+
 template <Layout LAY, typename K, typename V, int G, int MODE>
 __global__ void __launch_bounds__(256) k_insert(TableRef T, const K* __restrict__ keys,
                                                 const V* __restrict__ vals, uint64_t n,
@@ -46,7 +50,7 @@ __global__ void __launch_bounds__(256) k_insert(TableRef T, const K* __restrict_
                                                 int64_t* __restrict__ slot_out) {
   using P = Probe<LAY, K, V, G>;
   using Ops = typename P::Ops;
-  constexpr int CHUNK = chunk_for<K, V>();
+  constexpr int CHUNK = insert_chunk<K, V, MODE>();
   __shared__ ChunkState cs;
   __shared__ K s_keys[CHUNK];
   __shared__ uint32_t s_hw[CHUNK], s_sw[CHUNK];
@@ -58,10 +62,61 @@ __global__ void __launch_bounds__(256) k_insert(TableRef T, const K* __restrict_
   constexpr int lane = 0;  // one thread per key (probe.cuh)
   long long occ = 0, tomb = 0, ops = 0, att = 0, win = 0;
 
+  __shared__ uint16_t q_li[CHUNK];
+  __shared__ uint8_t q_o[CHUNK];
+  __shared__ uint32_t q_cnt;
+  using F = FastSpan<LAY, K, V>;
+
   while (chunk_begin<CHUNK>(cs, T.work, n)) {
+    if (threadIdx.x == 0) q_cnt = 0;
     stage_keys(s_keys, ss, keys, cs, T);
     if (MODE == 0) stage_in(s_vals, vals, cs);
     __syncthreads();
+
+    // ---- fast pass: one 128 B step per key; claims the first slot when it is an
+    // empty with no tombstone before it (the common case), otherwise queues the key
+    for (uint32_t fi = threadIdx.x; fi < cs.cnt; fi += blockDim.x) {
+      const K fkey = s_keys[fi];
+      if (fkey == (K)T.e || fkey == (K)T.t) {  // INVALID_KEY, no accounting (single_table.py:369-370)
+        s_status[fi] = ST_INVALID;
+        if (MODE == 1) s_slot[fi] = -1;
+        continue;
+      }
+      const ProbeStart fps = ss.get(fi);
+      F fs;
+      uint32_t o_next = 0;
+      if (fs.load(T, fps.h, fkey)) {
+        const uint32_t kb = fs.km & below_lowest(fs.em);
+        int res = OUT_NONE;
+        uint32_t u = 0;
+        if (kb) {
+          u = lowest_bit(kb);
+          res = OUT_FOUND;
+        } else if (fs.em && !(fs.tm & below_lowest(fs.em))) {
+          u = lowest_bit(fs.em);
+          bool won = false;
+          const K seen = Ops::claim(T, fs.base + u, (K)T.e, fkey, MODE == 0 ? s_vals[fi] : (V)0, MODE == 0, &won);
+          if (won) res = OUT_CLAIMED;
+          else if (seen == fkey) res = OUT_FOUND;
+        } else if (!fs.em && !fs.tm) {
+          o_next = fs.n_use;  // nothing free and no key in the span: continue after it
+        }
+        if (res != OUT_NONE) {
+          ops += 1;
+          att += (long long)chunk_end(u - fs.lo, G);
+          win += 1;
+          s_status[fi] = res == OUT_CLAIMED ? ST_INSERTED : ST_DUPLICATE;
+          if (MODE == 1) s_slot[fi] = (int64_t)(fs.base + u);
+          if (res == OUT_CLAIMED) occ += 1;
+          continue;
+        }
+      }
+      const uint32_t qi = atomicAdd(&q_cnt, 1u);
+      q_li[qi] = (uint16_t)fi;
+      q_o[qi] = (uint8_t)o_next;
+    }
+    __syncthreads();
+    const uint32_t nq = q_cnt;
 
     bool active = false;
     uint32_t li = 0;
@@ -73,21 +128,21 @@ __global__ void __launch_bounds__(256) k_insert(TableRef T, const K* __restrict_
     int64_t pending = -1;
     for (;;) {
       if (!active) {
-        for (;;) {
-          li = atomicAdd(&cs.next, 1u);
-          if (li >= cs.cnt) break;
-          key = s_keys[li];
-          if (key != (K)T.e && key != (K)T.t) break;
-          if (lane == 0) {  // sentinel keys: INVALID_KEY, no accounting (single_table.py:369-370)
-            s_status[li] = ST_INVALID;
-            if (MODE == 1) s_slot[li] = -1;
-          }
-        }
-        if (li >= cs.cnt) break;
+        const uint32_t qi = atomicAdd(&cs.next, 1u);
+        if (qi >= nq) break;
+        li = q_li[qi];
+        key = s_keys[li];
         if (MODE == 0) val = s_vals[li];
         ps = ss.get(li);
-        cur.init(ps.h);
         pending = -1;
+        if (!cursor_seek(T, cur, ps.h, ps.step, q_o[qi])) {  // budget spent without a free slot
+          ops += 1;
+          att += (long long)cur.attempts;
+          win += (long long)cur.windows_seen;
+          s_status[li] = ST_TABLE_FULL;
+          if (MODE == 1) s_slot[li] = -1;
+          continue;
+        }
         active = true;
       }
 
@@ -192,6 +247,10 @@ __global__ void __launch_bounds__(256) k_insert(TableRef T, const K* __restrict_
 // MODE 0: retrieve_bulk (single_table.py:376-408): value + found flag
 // MODE 1: find (slot_of / retrieve_with_stats, :317-336): slot, attempts, windows, value
 // MODE 2: erase (:338-351): retire the key (layout.py:224-243)
+//
+// Per chunk: a SIMT-uniform fast pass resolves every key whose answer lies in
+// the first 128 B of window 0 (FastSpan); the rest are queued and finished by
+// the flattened general loop.
 template <Layout LAY, typename K, typename V, int G, int MODE>
 __global__ void __launch_bounds__(256) k_lookup(TableRef T, const K* __restrict__ keys, uint64_t n,
                                                 V* __restrict__ vals_out, uint8_t* __restrict__ flag,
@@ -199,7 +258,7 @@ __global__ void __launch_bounds__(256) k_lookup(TableRef T, const K* __restrict_
                                                 uint32_t* __restrict__ att_out,
                                                 uint32_t* __restrict__ win_out) {
   using P = Probe<LAY, K, V, G>;
-  using Ops = typename P::Ops;
+  using F = FastSpan<LAY, K, V>;
   constexpr int CH = MODE == 1 ? CHUNK_FIND : chunk_for<K, V>();
   __shared__ ChunkState cs;
   __shared__ K s_keys[CH];
@@ -211,38 +270,90 @@ __global__ void __launch_bounds__(256) k_lookup(TableRef T, const K* __restrict_
   __shared__ int64_t s_slot[MODE == 1 ? CH : 1];
   __shared__ uint32_t s_att[MODE == 1 ? CH : 1];
   __shared__ uint32_t s_win[MODE == 1 ? CH : 1];
-  constexpr int lane = 0;  // one thread per key (probe.cuh)
+  __shared__ uint16_t q_li[CH];
+  __shared__ uint8_t q_o[CH];
+  __shared__ uint32_t q_cnt;
   long long ops = 0, att = 0, win = 0, occ = 0, tomb = 0;
 
+  // record the outcome of one key (found at slot `slot` / absent), `attempts` in g-units
+  auto finish = [&](uint32_t li, bool found, uint64_t slot, V value, bool erased, uint64_t attempts,
+                    uint64_t windows) {
+    if (MODE == 0) {
+      s_vals[li] = found ? value : (V)0;
+      s_flag[li] = (uint8_t)found;
+    } else if (MODE == 1) {
+      s_vals[li] = found ? value : (V)0;
+      s_slot[li] = found ? (int64_t)slot : -1;
+      s_att[li] = (uint32_t)attempts;
+      s_win[li] = (uint32_t)windows;
+    } else {
+      s_flag[li] = erased;
+      if (erased) { occ -= 1; tomb += 1; }
+    }
+    ops += 1;
+    att += (long long)attempts;
+    win += (long long)windows;
+  };
+
   while (chunk_begin<CH>(cs, T.work, n)) {
+    if (threadIdx.x == 0) q_cnt = 0;
     stage_keys(s_keys, ss, keys, cs, T);
     __syncthreads();
+
+    // ---- fast pass: one 128 B step for every key of the chunk
+    for (uint32_t li = threadIdx.x; li < cs.cnt; li += blockDim.x) {
+      const K key = s_keys[li];
+      if (key == (K)T.e || key == (K)T.t) {
+        if (MODE == 0) { ops += 1; s_vals[li] = 0; s_flag[li] = 0; }  // retrieve_bulk counts every query (:403)
+        if (MODE == 1) { s_slot[li] = -1; s_att[li] = 0; s_win[li] = 0; s_vals[li] = 0; }
+        if (MODE == 2) s_flag[li] = 0;
+        continue;
+      }
+      const ProbeStart ps = ss.get(li);
+      F fs;
+      uint32_t o_next = 0;
+      if (fs.load(T, ps.h, key)) {
+        const uint32_t kb = fs.km & below_lowest(fs.em);
+        if (kb) {
+          const uint32_t u = lowest_bit(kb);
+          const bool erased = MODE == 2 ? fs.retire(T, u) : false;
+          finish(li, true, fs.base + u, MODE == 2 ? (V)0 : fs.value(T, u), erased,
+                 chunk_end(u - fs.lo, G), 1);
+          continue;
+        }
+        if (fs.em) {
+          finish(li, false, 0, (V)0, false, chunk_end(lowest_bit(fs.em) - fs.lo, G), 1);
+          continue;
+        }
+        o_next = fs.n_use;
+      }
+      const uint32_t qi = atomicAdd(&q_cnt, 1u);
+      q_li[qi] = (uint16_t)li;
+      q_o[qi] = (uint8_t)o_next;
+    }
+    __syncthreads();
+
+    // ---- general loop over the queued keys (flattened, one step per iteration)
     bool active = false;
     uint32_t li = 0;
     K key = 0;
     ProbeStart ps{0, 0};
     Cursor cur;
     cur.init(0);
+    const uint32_t nq = q_cnt;
     for (;;) {
       if (!active) {
-        for (;;) {
-          li = atomicAdd(&cs.next, 1u);
-          if (li >= cs.cnt) break;
-          key = s_keys[li];
-          if (key != (K)T.e && key != (K)T.t) break;
-          if (MODE == 0) ops += lane == 0;  // retrieve_bulk counts every query (:403)
-          if (lane == 0) {
-            if (MODE == 0) { s_vals[li] = 0; s_flag[li] = 0; }
-            if (MODE == 1) { s_slot[li] = -1; s_att[li] = 0; s_win[li] = 0; s_vals[li] = 0; }
-            if (MODE == 2) s_flag[li] = 0;
-          }
-        }
-        if (li >= cs.cnt) break;
+        uint32_t qi = atomicAdd(&cs.next, 1u);
+        if (qi >= nq) break;
+        li = q_li[qi];
+        key = s_keys[li];
         ps = ss.get(li);
-        cur.init(ps.h);
+        if (!cursor_seek(T, cur, ps.h, ps.step, q_o[qi])) {  // window budget spent: absent
+          finish(li, false, 0, (V)0, false, cur.attempts, cur.windows_seen);
+          continue;
+        }
         active = true;
       }
-
       typename P::Step st;
       P::load(T, cur, key, st);
       const uint32_t kb = st.km & below_lowest(st.em);
@@ -261,23 +372,9 @@ __global__ void __launch_bounds__(256) k_lookup(TableRef T, const K* __restrict_
         attempts = cur.attempts;
       }
       if (!done) continue;
-
-      if (MODE == 0 || MODE == 1) {
-        s_vals[li] = found ? P::value(T, st, u) : (V)0;
-        if (MODE == 0) s_flag[li] = (uint8_t)found;
-        if (MODE == 1 && lane == 0) {
-          s_slot[li] = found ? (int64_t)(st.base + u) : -1;
-          s_att[li] = (uint32_t)attempts;
-          s_win[li] = (uint32_t)cur.windows_seen;
-        }
-      } else {
-        const bool won = found && P::retire(T, st, u);
-        s_flag[li] = won;
-        if (won) { occ -= 1; tomb += 1; }
-      }
-      ops += 1;
-      att += (long long)attempts;
-      win += (long long)cur.windows_seen;
+      const bool erased = MODE == 2 && found ? P::retire(T, st, u) : false;
+      finish(li, found, st.base + u, (MODE != 2 && found) ? P::value(T, st, u) : (V)0, erased, attempts,
+             cur.windows_seen);
       active = false;
     }
     __syncthreads();
@@ -312,12 +409,12 @@ struct SingleKernels {
                     uint8_t* status, int64_t* slot_out, int mode) {
     if (mode == 0) {
       auto kern = k_insert<LAY, K, V, G, 0>;
-      return launch_chunked(lc, T, (const void*)kern, n, chunk_for<K, V>(), [&](dim3 g, dim3 b) {
+      return launch_chunked(lc, T, (const void*)kern, n, insert_chunk<K, V, 0>(), [&](dim3 g, dim3 b) {
         kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status, slot_out);
       });
     }
     auto kern = k_insert<LAY, K, V, G, 1>;
-    return launch_chunked(lc, T, (const void*)kern, n, chunk_for<K, V>(), [&](dim3 g, dim3 b) {
+    return launch_chunked(lc, T, (const void*)kern, n, insert_chunk<K, V, 1>(), [&](dim3 g, dim3 b) {
       kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status, slot_out);
     });
   }
