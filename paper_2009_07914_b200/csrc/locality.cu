@@ -20,7 +20,7 @@
 namespace chb {
 
 constexpr int LOC_THREADS = 256;
-constexpr int LOC_ITEMS = 32;
+constexpr int LOC_ITEMS = 16;
 constexpr uint32_t LOC_TILE = (uint32_t)LOC_THREADS * LOC_ITEMS;
 constexpr uint32_t LOC_MAX_REGIONS = 1024;
 
@@ -37,10 +37,16 @@ __global__ void __launch_bounds__(LOC_THREADS) k_loc_count(TableRef T, const K* 
   for (uint32_t r = threadIdx.x; r < regions; r += LOC_THREADS) cnt[r] = 0;
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * LOC_TILE;
-#pragma unroll 4
+  K k[LOC_ITEMS];
+#pragma unroll
+  for (int it = 0; it < LOC_ITEMS; ++it) {  // all loads in flight before any use
+    const uint64_t i = base + (uint64_t)it * LOC_THREADS + threadIdx.x;
+    k[it] = i < n ? keys[i] : K{};
+  }
+#pragma unroll
   for (int it = 0; it < LOC_ITEMS; ++it) {
     const uint64_t i = base + (uint64_t)it * LOC_THREADS + threadIdx.x;
-    if (i < n) atomicAdd(&cnt[region_of(T, keys[i], shift)], 1u);
+    if (i < n) atomicAdd(&cnt[region_of(T, k[it], shift)], 1u);
   }
   __syncthreads();
   for (uint32_t r = threadIdx.x; r < regions; r += LOC_THREADS) hist[(uint64_t)r * gridDim.x + blockIdx.x] = cnt[r];
@@ -102,15 +108,22 @@ __global__ void __launch_bounds__(LOC_THREADS) k_loc_scatter(TableRef T, const K
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * LOC_TILE;
   const uint32_t valid = (uint32_t)((n - base) < LOC_TILE ? (n - base) : LOC_TILE);
-#pragma unroll 4
+  K k[LOC_ITEMS];
+  V v[LOC_ITEMS];
+#pragma unroll
+  for (int it = 0; it < LOC_ITEMS; ++it) {  // all loads in flight before any use
+    const uint32_t li = (uint32_t)it * LOC_THREADS + threadIdx.x;
+    k[it] = li < valid ? keys[base + li] : K{};
+    if (vals) v[it] = li < valid ? vals[base + li] : V{};
+  }
+#pragma unroll
   for (int it = 0; it < LOC_ITEMS; ++it) {
     const uint32_t li = (uint32_t)it * LOC_THREADS + threadIdx.x;
     if (li < valid) {
-      const K key = keys[base + li];
-      const uint32_t r = region_of(T, key, shift);
+      const uint32_t r = region_of(T, k[it], shift);
       const uint32_t j = loff[r] + atomicAdd(&fill[r], 1u);
-      s_keys[j] = key;
-      if (vals) s_vals[j] = vals[base + li];
+      s_keys[j] = k[it];
+      if (vals) s_vals[j] = v[it];
       s_reg[j] = (uint16_t)r;
       inv[base + li] = (uint16_t)j;
     }

@@ -44,7 +44,7 @@ template <typename K, typename V, int MODE>
 constexpr int insert_chunk() { return MODE == 1 ? 1024 : chunk_for<K, V>(); }
 
 template <Layout LAY, typename K, typename V, int G, int MODE>
-__global__ void __launch_bounds__(256) k_insert(TableRef T, const K* __restrict__ keys,
+__global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restrict__ keys,
                                                 const V* __restrict__ vals, uint64_t n,
                                                 uint8_t* __restrict__ status,
                                                 int64_t* __restrict__ slot_out) {
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(256) k_insert(TableRef T, const K* __restrict_
 // the first 128 B of window 0 (FastSpan); the rest are queued and finished by
 // the flattened general loop.
 template <Layout LAY, typename K, typename V, int G, int MODE>
-__global__ void __launch_bounds__(256) k_lookup(TableRef T, const K* __restrict__ keys, uint64_t n,
+__global__ void __launch_bounds__(256, 4) k_lookup(TableRef T, const K* __restrict__ keys, uint64_t n,
                                                 V* __restrict__ vals_out, uint8_t* __restrict__ flag,
                                                 int64_t* __restrict__ slot_out,
                                                 uint32_t* __restrict__ att_out,
@@ -309,23 +309,23 @@ __global__ void __launch_bounds__(256) k_lookup(TableRef T, const K* __restrict_
         if (MODE == 2) s_flag[li] = 0;
         continue;
       }
-      const ProbeStart ps = ss.get(li);
-      F fs;
       uint32_t o_next = 0;
-      if (fs.load(T, ps.h, key)) {
-        const uint32_t kb = fs.km & below_lowest(fs.em);
-        if (kb) {
-          const uint32_t u = lowest_bit(kb);
-          const bool erased = MODE == 2 ? fs.retire(T, u) : false;
-          finish(li, true, fs.base + u, MODE == 2 ? (V)0 : fs.value(T, u), erased,
-                 chunk_end(u - fs.lo, G), 1);
-          continue;
+      {
+        F fs;
+        if (fs.load(T, ss.get(li).h, key)) {
+          const uint32_t kb = fs.km & below_lowest(fs.em);
+          if (kb) {
+            const uint32_t u = lowest_bit(kb);
+            const bool erased = MODE == 2 ? fs.retire(T, u) : false;
+            finish(li, true, fs.base + u, MODE == 2 ? (V)0 : fs.value(T, u), erased, chunk_end(u - fs.lo, G), 1);
+            continue;
+          }
+          if (fs.em) {
+            finish(li, false, 0, (V)0, false, chunk_end(lowest_bit(fs.em) - fs.lo, G), 1);
+            continue;
+          }
+          o_next = fs.n_use;
         }
-        if (fs.em) {
-          finish(li, false, 0, (V)0, false, chunk_end(lowest_bit(fs.em) - fs.lo, G), 1);
-          continue;
-        }
-        o_next = fs.n_use;
       }
       const uint32_t qi = atomicAdd(&q_cnt, 1u);
       q_li[qi] = (uint16_t)li;
