@@ -306,6 +306,22 @@ def main() -> None:
     ins_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
     ret_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
 
+    # schedule statistics (outside the timed region): keys the staged-region pass handed
+    # to the COPS probe kernels (window 0 could not decide them)
+    sched = None
+    if world == 1:
+        _lib.check(_lib.lib().ch_clear(table._dt.handle, stream.cuda_stream), "clear")
+        table.reset_probe_counters()
+        table.insert_device(keys, vals, status=status)
+        d_ins = table.deferred_count()
+        table.reset_probe_counters()
+        table.retrieve_device(keys, values_out=out_v, found_out=out_f)
+        c_ret = table.probe_counters()
+        sched = {"deferred_insert_frac": d_ins / n, "deferred_retrieve_frac": table.deferred_count() / n,
+                 "retrieve_mean_attempts": c_ret.attempts / max(1, c_ret.ops)}
+        st, v, f = status, out_v, out_f
+        torch.cuda.synchronize()
+
     # verification (outside the timed region): every key found with its value
     ok = bool((st == 0).all().item() and (f == 1).all().item() and (v == vals).all().item())
     t_max = torch.tensor([total_ms, ins_ms, ret_ms], dtype=torch.float64, device=dev)
@@ -399,6 +415,7 @@ def main() -> None:
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "bytes_per_op": kbytes, "ops_per_launch": keys_per_launch, "traffic": traffic,
                          "kernel_ms": kms},
+            "schedule": sched,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks.summary(),
             "verified": ok,
         }

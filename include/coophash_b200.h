@@ -70,6 +70,7 @@ typedef struct ch_stats {
   int64_t total_values; /* bucket list (bucket_list.py:200-202) */
   uint64_t pool_allocated; /* BucketPool.allocated (bucket_list.py:151-153) */
   uint64_t device_error;   /* sticky device error bits */
+  uint64_t deferred;       /* staged-region keys finished by the COPS probe kernels (csrc/staged.cu) */
 } ch_stats;
 
 const char* ch_last_error(void);
@@ -86,8 +87,10 @@ int ch_clear(ch_table* t, void* stream);               /* K0: every cell empty, 
 int ch_get_stats(ch_table* t, ch_stats* out);          /* synchronizes the table's work */
 int ch_reset_probe_counters(ch_table* t, void* stream); /* single_table.py:136-138 */
 int ch_synchronize(ch_table* t);
-/* region-ordered execution of big batches (csrc/locality.cu): 0 auto (table > 256 MiB and
- * n >= c/16), 1 never, 2 always.  Results are identical; only the schedule changes. */
+/* schedule of big bulk insert / retrieve batches: 0 auto (table > 256 MiB and n >= c/16:
+ * staged regions for packed tables, L2 region order otherwise), 1 direct probes, 2 L2 region
+ * order (csrc/locality.cu), 3 shared-memory staged regions (csrc/staged.cu; packed only, other
+ * layouts run direct).  Result semantics are identical; only the schedule changes. */
 int ch_set_locality(ch_table* t, int mode);
 /* CUDA-event timing of the table's probe kernels (insert / lookup / multi passes):
  * enable, then read each launch's device time in launch order (up to cap entries) and

@@ -33,6 +33,7 @@ class ch_stats(C.Structure):
         ("capacity", C.c_uint64), ("occupied", C.c_int64), ("tombstones", C.c_int64),
         ("ops", C.c_uint64), ("attempts", C.c_uint64), ("windows", C.c_uint64),
         ("total_values", C.c_int64), ("pool_allocated", C.c_uint64), ("device_error", C.c_uint64),
+        ("deferred", C.c_uint64),
     ]
 
 

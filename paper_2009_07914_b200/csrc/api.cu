@@ -51,6 +51,12 @@ int loc_partition(const Launch& lc, const TableRef& T, const LocPlan& p, int kby
                   size_t scratch_bytes);
 int loc_unpermute(const Launch& lc, const LocPlan& p, uint64_t n, const uint16_t* inv, void* scratch,
                   size_t scratch_bytes, const void* pa, void* oa, int abytes, const void* pb, void* ob, int bbytes);
+bool staged_supported(const TableRef& T, uint64_t n);
+size_t staged_scratch_bytes(const TableRef& T, uint64_t n);
+int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, const void* vals,
+                  uint64_t n, uint8_t* status, void* scratch);
+int staged_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
+                  void* vals_out, uint8_t* found, void* scratch);
 int bucket_walk(const Launch& lc, const BucketRef& B, int vbytes, const uint64_t* handles, uint64_t n,
                 const uint64_t* offsets, void* out);
 
@@ -77,7 +83,9 @@ struct ch_table {
   cudaEvent_t last = nullptr;
   std::mutex mu;
   int sms = 148;
-  int loc_mode = 0;  // 0 auto, 1 never, 2 always (region-ordered execution, locality.cu)
+  // big-batch schedule: 0 auto, 1 direct, 2 L2 region order (locality.cu),
+  // 3 shared-memory staged regions (staged.cu, packed 32|32 tables)
+  int loc_mode = 0;
   bool timing = false;
   KernelTimer timer;
 };
@@ -180,8 +188,13 @@ int slot_bytes_of(const ch_table* t) {
 
 // Region-ordered execution pays off once the table outgrows L2 and the batch
 // touches most of its lines (locality.cu).  Positions travel as uint32.
+bool use_staged(const ch_table* t, uint64_t n) {
+  if (t->cfg.layout != CH_PACKED || !staged_supported(t->T, n)) return false;
+  return t->loc_mode == 3;  // opt-in until it beats the L2 region order
+}
+
 bool use_locality(const ch_table* t, uint64_t n) {
-  if (n == 0 || n >= (1ull << 32) || t->loc_mode == 1) return false;
+  if (n == 0 || n >= (1ull << 32) || t->loc_mode == 1 || t->loc_mode == 3) return false;
   if (t->loc_mode == 2) return true;
   const uint64_t bytes = t->T.c * (uint64_t)slot_bytes_of(t);
   return bytes >= (256ull << 20) && n * 16 >= t->T.c;
@@ -201,6 +214,7 @@ __global__ void k_reset_probe(DevCounters* c) {
   c->ops = 0;
   c->attempts = 0;
   c->windows = 0;
+  c->deferred = 0;
 }
 
 // element transitions of layout.py:140-243 on one slot
@@ -425,7 +439,8 @@ int ch_kernel_time(ch_table* t, double* ms, uint64_t cap, uint64_t* launches) {
 }
 
 int ch_set_locality(ch_table* t, int mode) {
-  if (!t || mode < 0 || mode > 2) return fail(CH_EINVAL, "locality mode must be 0 (auto), 1 (off) or 2 (on)");
+  if (!t || mode < 0 || mode > 3)
+    return fail(CH_EINVAL, "schedule must be 0 (auto), 1 (direct), 2 (L2 region order) or 3 (staged regions)");
   std::lock_guard<std::mutex> lock(t->mu);
   t->loc_mode = mode;
   return CH_OK;
@@ -455,6 +470,7 @@ int ch_get_stats(ch_table* t, ch_stats* out) {
   out->total_values = c.total_values;
   out->pool_allocated = c.pool_used;
   out->device_error = c.error;
+  out->deferred = c.deferred;
   return CH_OK;
 }
 
@@ -472,6 +488,12 @@ int ch_insert(ch_table* t, const void* keys, const void* vals, uint64_t n, uint8
   if (t->cfg.kind != CH_SINGLE) return fail(CH_EINVAL, "ch_insert needs a single-value table");
   if (n && (!keys || !vals || !status)) return fail(CH_EINVAL, "null buffer");
   Ordered o(t, stream);
+  if (use_staged(t, n)) {
+    Scratch sc(o.s);
+    void* p = sc.get(staged_scratch_bytes(t->T, n));
+    if (!p) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+    return o.done(staged_insert(o.lc, t->T, t->ts, keys, vals, n, status, p));
+  }
   if (!use_locality(t, n)) return o.done(single_insert(o.lc, t->T, t->ts, keys, vals, n, status, nullptr, 0));
   const LocPlan p = loc_plan(t->T, n, slot_bytes_of(t));
   Scratch sc(o.s);
@@ -502,6 +524,12 @@ int ch_retrieve(ch_table* t, const void* keys, uint64_t n, void* vals_out, uint8
   if (t->cfg.kind != CH_SINGLE) return fail(CH_EINVAL, "ch_retrieve needs a single-value table");
   if (n && (!keys || !vals_out || !found)) return fail(CH_EINVAL, "null buffer");
   Ordered o(t, stream);
+  if (use_staged(t, n)) {
+    Scratch sc(o.s);
+    void* p = sc.get(staged_scratch_bytes(t->T, n));
+    if (!p) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+    return o.done(staged_lookup(o.lc, t->T, t->ts, keys, n, vals_out, found, p));
+  }
   if (!use_locality(t, n))
     return o.done(single_lookup(o.lc, t->T, t->ts, keys, n, vals_out, found, nullptr, nullptr, nullptr, 0));
   const LocPlan p = loc_plan(t->T, n, slot_bytes_of(t));

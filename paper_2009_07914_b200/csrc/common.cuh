@@ -42,6 +42,7 @@ struct DevCounters {
   long long total_values;   // bucket list
   unsigned long long pool_used;  // bucket list: successfully allocated slots
   unsigned long long error;      // sticky device error flags (bit 0: contention timeout)
+  unsigned long long deferred;   // staged keys finished by the COPS kernels (staged.cu)
 };
 
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t key) {
@@ -365,7 +366,7 @@ struct Cursor {
 // Reference-unit probe count (single_table.py:197): g-sized chunks from the
 // window start; an op that stops at in-window offset o in window j has probed
 // 32 j + (o / g + 1) g slots (plus whatever full windows it walked before).
-__device__ __forceinline__ uint64_t chunk_end(uint32_t o, uint32_t g) { return (uint64_t)(o / g + 1) * g; }
+__device__ __forceinline__ uint64_t chunk_end(uint32_t o, uint32_t g) { return (uint64_t)((o & ~(g - 1u)) + g); }  // g = 2^k
 
 // ------------------------------------------------------ CTA reductions
 template <typename X>

@@ -24,6 +24,13 @@ struct Launch {
   int device;
   int sms;
   KernelTimer* timer = nullptr;
+  // probe kernels over a device-counted list (staged.cu fallback): when set, the
+  // batch size is *n_dev (n is only the capacity) and results go to dst[out_idx[i]]
+  const unsigned long long* n_dev = nullptr;
+  const uint32_t* out_idx = nullptr;
+  // per-element in-window offset to resume at (WINDOW: window 0 is known to hold
+  // neither the key nor a free slot, so the probe starts at window 1)
+  const uint8_t* o_start = nullptr;
 };
 
 struct TypeSel {

@@ -88,4 +88,15 @@ __device__ __forceinline__ void stage_out(X* __restrict__ dst, const X* src, con
   for (uint32_t j = threadIdx.x; j < cs.cnt; j += blockDim.x) dst[cs.base + j] = src[j];
 }
 
+// Results of a device-counted list (staged.cu) go back to their owners' positions.
+template <typename X>
+__device__ __forceinline__ void stage_out_ix(X* __restrict__ dst, const X* src, const ChunkState& cs,
+                                             const uint32_t* __restrict__ ix) {
+  if (!ix) {
+    stage_out(dst, src, cs);
+    return;
+  }
+  for (uint32_t j = threadIdx.x; j < cs.cnt; j += blockDim.x) dst[ix[cs.base + j]] = src[j];
+}
+
 }  // namespace chb

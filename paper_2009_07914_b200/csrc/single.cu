@@ -47,7 +47,11 @@ template <Layout LAY, typename K, typename V, int G, int MODE>
 __global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restrict__ keys,
                                                 const V* __restrict__ vals, uint64_t n,
                                                 uint8_t* __restrict__ status,
-                                                int64_t* __restrict__ slot_out) {
+                                                int64_t* __restrict__ slot_out,
+                                                const unsigned long long* __restrict__ n_dev,
+                                                const uint32_t* __restrict__ out_idx,
+                                                const uint8_t* __restrict__ o_start) {
+  if (n_dev) n = *n_dev;
   using P = Probe<LAY, K, V, G>;
   using Ops = typename P::Ops;
   constexpr int CHUNK = insert_chunk<K, V, MODE>();
@@ -84,8 +88,8 @@ __global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restri
       }
       const ProbeStart fps = ss.get(fi);
       F fs;
-      uint32_t o_next = 0;
-      if (fs.load(T, fps.h, fkey)) {
+      uint32_t o_next = o_start ? (uint32_t)o_start[cs.base + fi] : 0u;
+      if (o_next == 0 && fs.load(T, fps.h, fkey)) {
         const uint32_t kb = fs.km & below_lowest(fs.em);
         int res = OUT_NONE;
         uint32_t u = 0;
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restri
       }
     }
     __syncthreads();
-    stage_out(status, s_status, cs);
+    stage_out_ix(status, s_status, cs, out_idx);
     if (MODE == 1) stage_out(slot_out, s_slot, cs);
   }
   const long long v[5] = {ops, att, win, occ, tomb};
@@ -256,7 +260,11 @@ __global__ void __launch_bounds__(256, 4) k_lookup(TableRef T, const K* __restri
                                                 V* __restrict__ vals_out, uint8_t* __restrict__ flag,
                                                 int64_t* __restrict__ slot_out,
                                                 uint32_t* __restrict__ att_out,
-                                                uint32_t* __restrict__ win_out) {
+                                                uint32_t* __restrict__ win_out,
+                                                const unsigned long long* __restrict__ n_dev,
+                                                const uint32_t* __restrict__ out_idx,
+                                                const uint8_t* __restrict__ o_start) {
+  if (n_dev) n = *n_dev;
   using P = Probe<LAY, K, V, G>;
   using F = FastSpan<LAY, K, V>;
   constexpr int CH = MODE == 1 ? CHUNK_FIND : chunk_for<K, V>();
@@ -309,8 +317,8 @@ __global__ void __launch_bounds__(256, 4) k_lookup(TableRef T, const K* __restri
         if (MODE == 2) s_flag[li] = 0;
         continue;
       }
-      uint32_t o_next = 0;
-      {
+      uint32_t o_next = o_start ? (uint32_t)o_start[cs.base + li] : 0u;
+      if (o_next == 0) {
         F fs;
         if (fs.load(T, ss.get(li).h, key)) {
           const uint32_t kb = fs.km & below_lowest(fs.em);
@@ -379,8 +387,8 @@ __global__ void __launch_bounds__(256, 4) k_lookup(TableRef T, const K* __restri
     }
     __syncthreads();
     if (MODE == 0) {
-      stage_out(vals_out, s_vals, cs);
-      stage_out(flag, s_flag, cs);
+      stage_out_ix(vals_out, s_vals, cs, out_idx);
+      stage_out_ix(flag, s_flag, cs, out_idx);
     } else if (MODE == 1) {
       stage_out(slot_out, s_slot, cs);
       if (att_out) stage_out(att_out, s_att, cs);
@@ -410,12 +418,14 @@ struct SingleKernels {
     if (mode == 0) {
       auto kern = k_insert<LAY, K, V, G, 0>;
       return launch_chunked(lc, T, (const void*)kern, n, insert_chunk<K, V, 0>(), [&](dim3 g, dim3 b) {
-        kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status, slot_out);
+        kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status, slot_out, lc.n_dev,
+                                     lc.out_idx, lc.o_start);
       });
     }
     auto kern = k_insert<LAY, K, V, G, 1>;
     return launch_chunked(lc, T, (const void*)kern, n, insert_chunk<K, V, 1>(), [&](dim3 g, dim3 b) {
-      kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status, slot_out);
+      kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status, slot_out, lc.n_dev,
+                                     lc.out_idx, lc.o_start);
     });
   }
   static int lookup(const Launch& lc, const TableRef& T, const void* keys, uint64_t n, void* vals_out,
@@ -424,7 +434,8 @@ struct SingleKernels {
   {                                                                                                    \
     auto kern = k_lookup<LAY, K, V, G, M>;                                                             \
     return launch_chunked(lc, T, (const void*)kern, n, CH, [&](dim3 g, dim3 b) {                       \
-      kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, (V*)vals_out, flag, slot_out, att_out, win_out); \
+      kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, (V*)vals_out, flag, slot_out, att_out, win_out,   \
+                                   lc.n_dev, lc.out_idx, lc.o_start);                                  \
     });                                                                                                \
   }
     if (mode == 0) CHB_LOOKUP(0, (chunk_for<K, V>()))

@@ -119,13 +119,20 @@ class _TableBase:
         s = self._dt.stats()
         return ProbeCounters(ops=int(s.ops), attempts=int(s.attempts), windows_visited=int(s.windows))
 
+    def deferred_count(self) -> int:
+        """Keys the staged-region pass (csrc/staged.cu) handed to the COPS probe kernels
+        since the last reset_probe_counters() (window 0 could not decide them)."""
+        return int(self._dt.stats().deferred)
+
     def reset_probe_counters(self) -> None:
         _lib.check(_lib.lib().ch_reset_probe_counters(self._dt.handle, self._stream()),
                    "reset_probe_counters")
 
     def set_locality(self, mode) -> None:
-        """Region-ordered execution of big batches: "auto" (default), "off" or "on"."""
-        code = {"auto": 0, "off": 1, "on": 2}.get(mode, mode)
+        """Schedule of big batches: "auto" (default), "off" (direct probes), "on" (L2 region
+        order, csrc/locality.cu) or "staged" (shared-memory staged regions, csrc/staged.cu;
+        packed tables, other layouts run direct)."""
+        code = {"auto": 0, "off": 1, "on": 2, "staged": 3}.get(mode, mode)
         _lib.check(_lib.lib().ch_set_locality(self._dt.handle, int(code)), "set_locality")
 
     def kernel_timing(self, enable: bool = True) -> None:

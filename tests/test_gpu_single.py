@@ -66,7 +66,7 @@ def test_sequential_replay_is_slot_exact(idx):
 
 # ------------------------------------------------ bulk replay: semantic parity
 
-@pytest.mark.parametrize("loc", ["off", "on"])
+@pytest.mark.parametrize("loc", ["off", "on", "staged"])
 @pytest.mark.parametrize("idx", range(11))
 def test_bulk_replay_semantics(idx, loc):
     sc = load("single.json")["scenarios"][idx]
@@ -119,7 +119,8 @@ def test_bulk_replay_semantics(idx, loc):
     ("soa", 64, 64, 4), ("soa", 32, 64, 8), ("soa", 64, 32, 16), ("soa", 32, 32, 32),
     ("aos", 64, 64, 8), ("aos", 32, 32, 4), ("aos", 32, 64, 2), ("aos", 64, 32, 1),
 ])
-@pytest.mark.parametrize("rho,loc", [(0.8, "auto"), (0.95, "auto"), (0.95, "on")])
+@pytest.mark.parametrize("rho,loc", [(0.8, "auto"), (0.95, "auto"), (0.95, "on"), (0.8, "staged"),
+                                     (0.95, "staged")])
 def test_bulk_unique_vs_oracle(layout, kb, vb, g, rho, loc):
     n = 1 << 18
     rng = np.random.default_rng(zlib.crc32(f"{layout}{kb}{vb}{g}{rho}{loc}".encode()))
@@ -304,7 +305,7 @@ def test_in_batch_duplicates():              # :190-197
     assert t.retrieve(5) in (1, 3, 4) and t.retrieve(6) in (2, 5)
 
 
-@pytest.mark.parametrize("loc", ["off", "on"])
+@pytest.mark.parametrize("loc", ["off", "on", "staged"])
 def test_same_key_storm_single_winner(loc):  # :278-298 (8 threads -> 1M lanes)
     t = SingleValueHashTable(256, layout="packed", key_bits=32, value_bits=32)
     t.set_locality(loc)
@@ -381,7 +382,7 @@ def test_locality_path_at_scale_matches_direct():
                             .view(np.int32)).cuda()
     vals = torch.arange(n, dtype=torch.int32, device="cuda")
     out = []
-    for loc in ("off", "on"):
+    for loc in ("off", "on", "staged"):
         t = SingleValueHashTable(int(n / 0.95), layout="packed", key_bits=32, value_bits=32, group_width=8)
         t.set_locality(loc)
         st = t.insert_device(keys, vals)
@@ -393,7 +394,82 @@ def test_locality_path_at_scale_matches_direct():
         assert f.bool().all().item() and (v == vals).all().item()
         miss = keys[: 1 << 20] ^ 0x5A5A5A5A
         out.append(t.retrieve_device(miss))
-    assert torch.equal(out[0][1], out[1][1]) and torch.equal(out[0][0], out[1][0])
+    for o in out[1:]:
+        assert torch.equal(out[0][1], o[1]) and torch.equal(out[0][0], o[0])
+
+
+@pytest.mark.parametrize("rho", [0.8, 0.95, 0.99])
+def test_staged_path_mixed_batches_vs_oracle(rho):
+    """Staged regions (csrc/staged.cu) on batches mixing new keys, in-batch duplicates,
+    keys already present, sentinels and tombstones: statuses, values and found flags
+    against the oracle's sequential semantics for the distinct-key parts."""
+    n = 1 << 20
+    rng = np.random.default_rng(int(rho * 100))
+    pool = rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=3 * n, dtype=np.uint64)))
+    first, second, absent = pool[:n // 2], pool[n // 2:n], pool[n:2 * n]
+    cap = int(np.ceil(n / rho))
+    t = SingleValueHashTable(cap, layout="packed", key_bits=32, value_bits=32, group_width=8)
+    t.set_locality("staged")
+    v1 = rng.integers(0, 1 << 32, size=first.size, dtype=np.uint64)
+    st = t.insert_device(first, v1).cpu().numpy()
+    assert (st == 0).all() and t.occupied == first.size
+    # erase a quarter: tombstones in front of later keys' first empties
+    gone = first[: first.size // 4]
+    er = t.erase_device(gone).cpu().numpy()
+    assert er.all() and t.tombstones == gone.size
+    # batch: second half new keys (+ a duplicated tail), old keys again, sentinels
+    dup = second[: 4096]
+    keys = np.concatenate([second, dup, first[first.size // 4:first.size // 4 + 8192],
+                           np.array([(1 << 32) - 1, (1 << 32) - 2], dtype=np.uint64)])
+    perm = rng.permutation(keys.size)
+    keys = keys[perm]
+    vals = rng.integers(0, 1 << 32, size=keys.size, dtype=np.uint64)
+    st = t.insert_device(keys, vals).cpu().numpy()
+    inv = keys >= (1 << 32) - 2
+    assert (st[inv] == 3).all()
+    ins = st == 0
+    ks, cnt = np.unique(keys[ins], return_counts=True)
+    assert (cnt == 1).all(), "two INSERTED for one key"
+    assert set(ks.tolist()) == set(second.tolist())
+    old = np.isin(keys, first)
+    assert (st[old] == 1).all()
+    winner = dict(zip(keys[ins].tolist(), vals[ins].tolist()))
+    model = dict(zip(first[first.size // 4:].tolist(), v1[first.size // 4:].tolist()))
+    model.update(winner)
+    assert t.occupied == len(model)
+    q = np.concatenate([np.array(list(model.keys()), dtype=np.uint64), gone, absent[: n // 2]])
+    q = q[rng.permutation(q.size)]
+    v, f = t.retrieve_device(q)
+    v = v.cpu().numpy().view(np.uint32).astype(np.uint64)
+    f = f.cpu().numpy().astype(bool)
+    want_f = np.isin(q, np.array(list(model.keys()), dtype=np.uint64))
+    assert (f == want_f).all()
+    want_v = np.array([model.get(int(k), 0) for k in q[f]], dtype=np.uint64)
+    assert (v[f] == want_v).all() and (v[~f] == 0).all()
+    # the staged lookup agrees with the direct one bit for bit
+    t.set_locality("off")
+    dv, df = t.retrieve_device(q)
+    assert (dv.cpu().numpy().view(np.uint32).astype(np.uint64) == v).all()
+    assert (df.cpu().numpy().astype(bool) == f).all()
+
+
+def test_staged_counters_match_direct_readonly():
+    """Read-only staged lookups count ops / attempts / windows exactly like direct probes."""
+    n = 1 << 20
+    rng = np.random.default_rng(5)
+    keys = rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=2 * n, dtype=np.uint64)))
+    present, absent = keys[:n], keys[n:2 * n]
+    t = SingleValueHashTable(int(n / 0.95), layout="packed", key_bits=32, value_bits=32, group_width=4)
+    t.insert_device(present, present)
+    q = np.concatenate([present, absent])
+    res = []
+    for loc in ("off", "staged"):
+        t.set_locality(loc)
+        t.reset_probe_counters()
+        t.retrieve_device(q)
+        c = t.probe_counters()
+        res.append((c.ops, c.attempts, c.windows_visited))
+    assert res[0] == res[1]
 
 
 def test_host_pipeline_matches_device_path():
