@@ -220,7 +220,7 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", default="", help="write a g x load sweep to this JSON file")
-    ap.add_argument("--locality", default="auto", choices=("auto", "on", "off"),
+    ap.add_argument("--locality", default="auto", choices=("auto", "on", "off", "staged"),
                     help="region-ordered execution of the batch (csrc/locality.cu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup

@@ -52,7 +52,7 @@ int loc_partition(const Launch& lc, const TableRef& T, const LocPlan& p, int kby
 int loc_unpermute(const Launch& lc, const LocPlan& p, uint64_t n, const uint16_t* inv, void* scratch,
                   size_t scratch_bytes, const void* pa, void* oa, int abytes, const void* pb, void* ob, int bbytes);
 bool staged_supported(const TableRef& T, uint64_t n);
-size_t staged_scratch_bytes(const TableRef& T, uint64_t n);
+size_t staged_scratch_bytes(const TableRef& T, uint64_t n, bool insert);
 int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, const void* vals,
                   uint64_t n, uint8_t* status, void* scratch);
 int staged_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
@@ -190,7 +190,10 @@ int slot_bytes_of(const ch_table* t) {
 // touches most of its lines (locality.cu).  Positions travel as uint32.
 bool use_staged(const ch_table* t, uint64_t n) {
   if (t->cfg.layout != CH_PACKED || !staged_supported(t->T, n)) return false;
-  return t->loc_mode == 3;  // opt-in until it beats the L2 region order
+  if (t->loc_mode == 3) return true;
+  if (t->loc_mode != 0) return false;
+  const uint64_t bytes = t->T.c * 8ull;  // a table larger than L2, a batch covering it
+  return bytes >= (256ull << 20) && n * 16 >= t->T.c;
 }
 
 bool use_locality(const ch_table* t, uint64_t n) {
@@ -490,7 +493,7 @@ int ch_insert(ch_table* t, const void* keys, const void* vals, uint64_t n, uint8
   Ordered o(t, stream);
   if (use_staged(t, n)) {
     Scratch sc(o.s);
-    void* p = sc.get(staged_scratch_bytes(t->T, n));
+    void* p = sc.get(staged_scratch_bytes(t->T, n, true));
     if (!p) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
     return o.done(staged_insert(o.lc, t->T, t->ts, keys, vals, n, status, p));
   }
@@ -526,7 +529,7 @@ int ch_retrieve(ch_table* t, const void* keys, uint64_t n, void* vals_out, uint8
   Ordered o(t, stream);
   if (use_staged(t, n)) {
     Scratch sc(o.s);
-    void* p = sc.get(staged_scratch_bytes(t->T, n));
+    void* p = sc.get(staged_scratch_bytes(t->T, n, false));
     if (!p) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
     return o.done(staged_lookup(o.lc, t->T, t->ts, keys, n, vals_out, found, p));
   }

@@ -177,18 +177,19 @@ struct FastSpan {
 
 // Position a fresh cursor (window 0 at h) at in-window offset o; returns false
 // if that exhausts the window budget.
+// (o < 2 WINDOW: the fast pass examines at most window 0 or the start of window 1)
 __device__ __forceinline__ bool cursor_seek(const TableRef& T, Cursor& cur, uint64_t h, uint64_t step, uint32_t o) {
   cur.init(h);
-  cur.o = o;
-  if (o == WINDOW) {
+  while (o >= WINDOW) {
     cur.attempts += WINDOW;
-    cur.j = 1;
+    cur.j += 1;
     if (cur.j >= T.max_windows) return false;
-    cur.windows_seen = 2;
+    cur.windows_seen += 1;
     cur.ws += step;
     if (cur.ws >= T.c) cur.ws -= T.c;
-    cur.o = 0;
+    o -= WINDOW;
   }
+  cur.o = o;
   return true;
 }
 

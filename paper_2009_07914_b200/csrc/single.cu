@@ -88,8 +88,17 @@ __global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restri
       }
       const ProbeStart fps = ss.get(fi);
       F fs;
-      uint32_t o_next = o_start ? (uint32_t)o_start[cs.base + fi] : 0u;
-      if (o_next == 0 && fs.load(T, fps.h, fkey)) {
+      // o0 = WINDOW: the staged pass saw window 0 hold neither the key nor a free
+      // cell, so the fast span runs at window 1's start (staged.cu)
+      const uint32_t o0 = o_start ? (uint32_t)o_start[cs.base + fi] : 0u;
+      const uint32_t jw = o0 ? 1u : 0u;
+      uint32_t o_next = o0;
+      uint64_t fws = fps.h;
+      if (jw) {
+        fws += fps.step;
+        if (fws >= T.c) fws -= T.c;
+      }
+      if ((o0 == 0 || (o0 == WINDOW && T.max_windows > 1)) && fs.load(T, fws, fkey)) {
         const uint32_t kb = fs.km & below_lowest(fs.em);
         int res = OUT_NONE;
         uint32_t u = 0;
@@ -103,12 +112,12 @@ __global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restri
           if (won) res = OUT_CLAIMED;
           else if (seen == fkey) res = OUT_FOUND;
         } else if (!fs.em && !fs.tm) {
-          o_next = fs.n_use;  // nothing free and no key in the span: continue after it
+          o_next = o0 + fs.n_use;  // nothing free and no key in the span: continue after it
         }
         if (res != OUT_NONE) {
           ops += 1;
-          att += (long long)chunk_end(u - fs.lo, G);
-          win += 1;
+          att += (long long)(jw * WINDOW + chunk_end(u - fs.lo, G));
+          win += 1 + jw;
           s_status[fi] = res == OUT_CLAIMED ? ST_INSERTED : ST_DUPLICATE;
           if (MODE == 1) s_slot[fi] = (int64_t)(fs.base + u);
           if (res == OUT_CLAIMED) occ += 1;
@@ -317,22 +326,33 @@ __global__ void __launch_bounds__(256, 4) k_lookup(TableRef T, const K* __restri
         if (MODE == 2) s_flag[li] = 0;
         continue;
       }
-      uint32_t o_next = o_start ? (uint32_t)o_start[cs.base + li] : 0u;
-      if (o_next == 0) {
+      // o0 = WINDOW: window 0 is known to hold neither the key nor an empty (staged.cu):
+      // the fast span runs at window 1's start
+      const uint32_t o0 = o_start ? (uint32_t)o_start[cs.base + li] : 0u;
+      uint32_t o_next = o0;
+      if (o0 == 0 || (o0 == WINDOW && T.max_windows > 1)) {
+        const uint32_t jw = o0 ? 1u : 0u;
+        const ProbeStart fps = ss.get(li);
+        uint64_t fws = fps.h;
+        if (jw) {
+          fws += fps.step;
+          if (fws >= T.c) fws -= T.c;
+        }
         F fs;
-        if (fs.load(T, ss.get(li).h, key)) {
+        if (fs.load(T, fws, key)) {
           const uint32_t kb = fs.km & below_lowest(fs.em);
           if (kb) {
             const uint32_t u = lowest_bit(kb);
             const bool erased = MODE == 2 ? fs.retire(T, u) : false;
-            finish(li, true, fs.base + u, MODE == 2 ? (V)0 : fs.value(T, u), erased, chunk_end(u - fs.lo, G), 1);
+            finish(li, true, fs.base + u, MODE == 2 ? (V)0 : fs.value(T, u), erased,
+                   jw * WINDOW + chunk_end(u - fs.lo, G), 1 + jw);
             continue;
           }
           if (fs.em) {
-            finish(li, false, 0, (V)0, false, chunk_end(lowest_bit(fs.em) - fs.lo, G), 1);
+            finish(li, false, 0, (V)0, false, jw * WINDOW + chunk_end(lowest_bit(fs.em) - fs.lo, G), 1 + jw);
             continue;
           }
-          o_next = fs.n_use;
+          o_next = o0 + fs.n_use;
         }
       }
       const uint32_t qi = atomicAdd(&q_cnt, 1u);
