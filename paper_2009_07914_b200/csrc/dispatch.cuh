@@ -30,7 +30,10 @@ struct Launch {
   const uint32_t* out_idx = nullptr;
   // per-element in-window offset to resume at (WINDOW: window 0 is known to hold
   // neither the key nor a free slot, so the probe starts at window 1)
-  const uint8_t* o_start = nullptr;
+  const uint32_t* o_start = nullptr;
+  // cap on the CTAs of a chunk-scheduled kernel (0: one full wave).  A narrower
+  // wave keeps the in-flight band of a region-ordered batch inside L2.
+  int max_blocks = 0;
 };
 
 struct TypeSel {
@@ -88,7 +91,8 @@ int launch_chunked(const Launch& lc, const TableRef& T, const void* kern, uint64
   int rc = cuda_check(cudaMemsetAsync(T.work, 0, sizeof(unsigned long long), lc.stream), "queue reset");
   if (rc) return rc;
   const uint64_t want = (items + chunk - 1) / chunk;
-  const uint64_t full = (uint64_t)lc.sms * (uint64_t)occupancy(kern, threads);
+  uint64_t full = (uint64_t)lc.sms * (uint64_t)occupancy(kern, threads);
+  if (lc.max_blocks > 0 && (uint64_t)lc.max_blocks < full) full = (uint64_t)lc.max_blocks;
   const uint64_t blocks = want < full ? want : full;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (lc.timer && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess)

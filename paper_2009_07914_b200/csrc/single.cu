@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restri
                                                 int64_t* __restrict__ slot_out,
                                                 const unsigned long long* __restrict__ n_dev,
                                                 const uint32_t* __restrict__ out_idx,
-                                                const uint8_t* __restrict__ o_start) {
+                                                const uint32_t* __restrict__ o_start) {
   if (n_dev) n = *n_dev;
   using P = Probe<LAY, K, V, G>;
   using Ops = typename P::Ops;
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restri
       F fs;
       // o0 = WINDOW: the staged pass saw window 0 hold neither the key nor a free
       // cell, so the fast span runs at window 1's start (staged.cu)
-      const uint32_t o0 = o_start ? (uint32_t)o_start[cs.base + fi] : 0u;
+      const uint32_t o0 = o_start ? o_start[cs.base + fi] : 0u;
       const uint32_t jw = o0 ? 1u : 0u;
       uint32_t o_next = o0;
       uint64_t fws = fps.h;
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256, 4) k_lookup(TableRef T, const K* __restri
                                                 uint32_t* __restrict__ win_out,
                                                 const unsigned long long* __restrict__ n_dev,
                                                 const uint32_t* __restrict__ out_idx,
-                                                const uint8_t* __restrict__ o_start) {
+                                                const uint32_t* __restrict__ o_start) {
   if (n_dev) n = *n_dev;
   using P = Probe<LAY, K, V, G>;
   using F = FastSpan<LAY, K, V>;
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(256, 4) k_lookup(TableRef T, const K* __restri
       }
       // o0 = WINDOW: window 0 is known to hold neither the key nor an empty (staged.cu):
       // the fast span runs at window 1's start
-      const uint32_t o0 = o_start ? (uint32_t)o_start[cs.base + li] : 0u;
+      const uint32_t o0 = o_start ? o_start[cs.base + li] : 0u;
       uint32_t o_next = o0;
       if (o0 == 0 || (o0 == WINDOW && T.max_windows > 1)) {
         const uint32_t jw = o0 ? 1u : 0u;

@@ -32,6 +32,8 @@
 // (bucket, tile) runs, and records where each element went (u16 rank inside the
 // tile, per-tile run table), so results return by gathering the same runs --
 // every pass reads and writes coalesced and no position is carried per key.
+#include <cstdlib>
+
 #include "dispatch.cuh"
 
 namespace chb {
@@ -46,8 +48,18 @@ constexpr uint32_t PBINS = 512;
 constexpr int RT = 256;                    // region CTA threads
 constexpr uint32_t ST_MAX_REGIONS = 51200; // count histogram in shared memory (200 KiB)
 
-__device__ __forceinline__ uint32_t region_of_key(const TableRef& T, uint32_t key) {
-  return (uint32_t)(T.modc.mod(mix64((uint64_t)key)) >> ST_LOG_R);
+// Start slot of window wj (0 or 1) of key's COPS sequence: h, or h + step mod c
+// (probing.py:202-220; step = 32 (1 + stephash mod (p-1)), p = 2 -> 32).  c < 2^32.
+__device__ __forceinline__ uint32_t window_start(const TableRef& T, uint32_t key, int wj) {
+  uint64_t ws = T.modc.mod(mix64((uint64_t)key));
+  if (wj) {
+    ws += T.p == 2 ? (uint64_t)WINDOW : (uint64_t)WINDOW * (1 + T.modpm1.mod(mix64(STEP_SEED ^ (uint64_t)key)));
+    if (ws >= T.c) ws -= T.c;
+  }
+  return (uint32_t)ws;
+}
+__device__ __forceinline__ uint32_t region_of_key(const TableRef& T, uint32_t key, int wj) {
+  return window_start(T, key, wj) >> ST_LOG_R;
 }
 
 // ------------------------------------------------------------- TMA helpers
@@ -91,8 +103,10 @@ __device__ __forceinline__ void fence_smem_to_async() { asm volatile("fence.prox
 // ------------------------------------------------------------- count
 // Region histogram of the batch (dynamic shared memory, one counter per region).
 __global__ void __launch_bounds__(1024) k_st_count(TableRef T, const uint32_t* __restrict__ keys, uint64_t n,
-                                                   uint32_t regions, uint32_t* __restrict__ gcount) {
+                                                   uint32_t regions, uint32_t* __restrict__ gcount,
+                                                   const unsigned long long* __restrict__ n_dev, int wj) {
   extern __shared__ uint32_t s_cnt[];
+  if (n_dev) n = *n_dev;
   for (uint32_t i = threadIdx.x; i < regions; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -102,9 +116,9 @@ __global__ void __launch_bounds__(1024) k_st_count(TableRef T, const uint32_t* _
 #pragma unroll
     for (int u = 0; u < 4; ++u) k[u] = __ldcs(keys + i + u * stride);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) atomicAdd(&s_cnt[region_of_key(T, k[u])], 1u);
+    for (int u = 0; u < 4; ++u) atomicAdd(&s_cnt[region_of_key(T, k[u], wj)], 1u);
   }
-  for (; i < n; i += stride) atomicAdd(&s_cnt[region_of_key(T, keys[i])], 1u);
+  for (; i < n; i += stride) atomicAdd(&s_cnt[region_of_key(T, keys[i], wj)], 1u);
   __syncthreads();
   for (uint32_t r = threadIdx.x; r < regions; r += blockDim.x)
     if (s_cnt[r]) atomicAdd(&gcount[r], s_cnt[r]);
@@ -212,21 +226,35 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // bucketed keys (+ values, + the window start inside the region at level 2) it
 // records the inverse: inv[pos] = the element's slot in the tile's bucketed
 // order, th/tg[t * nb + b] = length / destination of the tile's run of bucket b.
-template <int L, bool VALS>
+// NPAY u32 payload arrays ride along (0: lookup keys, 1: + values, 2: + the
+// round-1 position of a round-2 key, or of a lookup key in round 2 with NPAY=1
+// meaning the position).  Round 2 (wj = 1) partitions the deferred keys by their
+// window-1 start; its count lives on the device (n_dev) and it needs no inverse.
+template <int L, int NPAY>
 __global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, const uint64_t* __restrict__ foff,
                                                     const uint32_t* __restrict__ tstart, uint32_t supers,
                                                     uint32_t regions, uint32_t ntiles,
                                                     const uint32_t* __restrict__ kin,
-                                                    const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
-                                                    uint32_t* __restrict__ vout, uint16_t* __restrict__ lo_out,
-                                                    uint16_t* __restrict__ inv, uint16_t* __restrict__ th,
-                                                    uint32_t* __restrict__ tg, uint32_t nb,
-                                                    uint32_t* __restrict__ cursor) {
+                                                    const uint32_t* __restrict__ vin,
+                                                    const uint32_t* __restrict__ pin,
+                                                    const uint32_t* __restrict__ rin, uint32_t* __restrict__ kout,
+                                                    uint32_t* __restrict__ vout, uint32_t* __restrict__ pout,
+                                                    uint32_t* __restrict__ rout,
+                                                    uint16_t* __restrict__ lo_out, uint16_t* __restrict__ inv,
+                                                    uint16_t* __restrict__ th, uint32_t* __restrict__ tg, uint32_t nb,
+                                                    uint32_t* __restrict__ cursor,
+                                                    const unsigned long long* __restrict__ n_dev, int wj) {
+  constexpr bool VALS = NPAY >= 1;
+  constexpr bool POS = NPAY >= 2;
+  constexpr bool RES = NPAY >= 3;
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* sK = reinterpret_cast<uint32_t*>(smem);
   uint32_t* sV = sK + PTILE;
-  uint16_t* sD = reinterpret_cast<uint16_t*>(sV + (VALS ? PTILE : 0));
+  uint32_t* sP = sV + (VALS ? PTILE : 0);
+  uint32_t* sR = sP + (POS ? PTILE : 0);
+  uint16_t* sD = reinterpret_cast<uint16_t*>(sR + (RES ? PTILE : 0));
   uint16_t* sL = sD + PTILE;  // level 2 only
+  if (n_dev) n = *n_dev;
   __shared__ uint32_t hist[PBINS], boff[PBINS], gbase[PBINS];
   __shared__ uint32_t wt[PT / 32];
   const uint32_t t = blockIdx.x;
@@ -238,19 +266,21 @@ __global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, cons
   TileGeo g;
   if (t >= ntiles || !tile_geo<L>(t, n, foff, s_ts, supers, regions, g)) return;
   hist[threadIdx.x] = 0;  // PBINS == PT
-  uint32_t k[PI], v[PI], d[PI], r[PI];
+  uint32_t k[PI], v[PI], q[PI], w[PI], d[PI], r[PI];
 #pragma unroll
   for (int it = 0; it < PI; ++it) {  // all loads in flight before any use
     const uint32_t li = (uint32_t)it * PT + threadIdx.x;
     k[it] = li < g.cnt ? __ldcs(kin + g.pos0 + li) : 0u;
     if (VALS) v[it] = li < g.cnt ? __ldcs(vin + g.pos0 + li) : 0u;
+    if (POS) q[it] = li < g.cnt ? __ldcs(pin + g.pos0 + li) : 0u;
+    if (RES) w[it] = li < g.cnt ? __ldcs(rin + g.pos0 + li) : 0u;
   }
   __syncthreads();  // hist zeroed
 #pragma unroll
   for (int it = 0; it < PI; ++it) {
     const uint32_t li = (uint32_t)it * PT + threadIdx.x;
     if (li >= g.cnt) continue;
-    const uint32_t h = (uint32_t)T.modc.mod(mix64((uint64_t)k[it]));  // c < 2^32
+    const uint32_t h = window_start(T, k[it], wj);
     const uint32_t b = L == 1 ? (h >> ST_LOG_R) >> ST_S2 : (h >> ST_LOG_R) - g.cbase;
     r[it] = atomicAdd(&hist[b], 1u);
     d[it] = b | (L == 2 ? (h & (ST_R - 1)) << 16 : 0u);  // window start rides along (registers)
@@ -261,7 +291,7 @@ __global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, cons
   boff[threadIdx.x] = bo;
   const uint32_t gb = hv ? atomicAdd(&cursor[g.cbase + threadIdx.x], hv) : 0u;
   gbase[threadIdx.x] = gb;
-  if (threadIdx.x < nb) {
+  if (th && threadIdx.x < nb) {
     th[(uint64_t)t * nb + threadIdx.x] = (uint16_t)hv;
     tg[(uint64_t)t * nb + threadIdx.x] = gb;
   }
@@ -274,9 +304,11 @@ __global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, cons
     const uint32_t j = boff[b] + r[it];
     sK[j] = k[it];
     if (VALS) sV[j] = v[it];
+    if (POS) sP[j] = q[it];
+    if (RES) sR[j] = w[it];
     sD[j] = (uint16_t)b;
     if (L == 2) sL[j] = (uint16_t)(d[it] >> 16);
-    inv[g.pos0 + li] = (uint16_t)j;
+    if (inv) inv[g.pos0 + li] = (uint16_t)j;
   }
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < g.cnt; j += PT) {
@@ -284,6 +316,8 @@ __global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, cons
     const uint32_t dst = gbase[b] + (j - boff[b]);
     kout[dst] = sK[j];
     if (VALS) vout[dst] = sV[j];
+    if (POS) pout[dst] = sP[j];
+    if (RES) rout[dst] = sR[j];
     if (L == 2) lo_out[dst] = sL[j];
   }
 }
@@ -384,7 +418,7 @@ struct DeferBuf {
 
 struct DeferOut {
   uint32_t *k, *v, *x;
-  uint8_t* o;
+  uint32_t* o;
   unsigned long long* count;
 };
 
@@ -402,7 +436,7 @@ __device__ __forceinline__ void defer_push(DeferBuf<VALS, CAP>& B, const DeferOu
     D.k[g] = k;
     if (VALS) D.v[g] = v;
     D.x[g] = x;
-    D.o[g] = (uint8_t)o;
+    D.o[g] = o;
   }
 }
 
@@ -456,22 +490,31 @@ __device__ __forceinline__ void queue_push(bool push, uint16_t e, uint16_t* q, u
 // another key of the round -- are compacted into the next round's queue.  A
 // thread-per-key loop over the whole window ran at ~7 of 32 active lanes (the
 // warp waited on its longest probe; profiles/r01_region_v3).
-template <int MODE>
+// R2 (round 2): the keys are round 1's deferred ones, probed in window 1, and each
+// carries the position its result belongs to (pos).  Deferrals go to DA when the
+// COPS kernel must re-examine the window (start crossing the region end, a
+// tombstone before the first empty) and to DB when the window is full (round 1:
+// those are round 2's input; round 2: DB == DA, the COPS kernel's list).
+template <int MODE, bool R2>
 __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* __restrict__ foff,
                                                     const uint32_t* __restrict__ keys,
                                                     const uint32_t* __restrict__ vals,
+                                                    const uint32_t* __restrict__ pos,
                                                     const uint16_t* __restrict__ los, uint8_t* __restrict__ status,
                                                     uint32_t* __restrict__ res_val, uint8_t* __restrict__ res_flag,
-                                                    DeferOut D, int g) {
+                                                    DeferOut DA, DeferOut DB, int g) {
   constexpr bool INS = MODE == 0;
   constexpr uint32_t HALO = INS ? 0u : ST_HALO;
+  constexpr uint32_t OW = R2 ? WINDOW : 0u;  // sequence offset of the window probed here
   extern __shared__ __align__(128) unsigned char dsm[];
   uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
   uint32_t* s_key = reinterpret_cast<uint32_t*>(tile + ST_R + HALO + TILE_PAD);
   uint32_t* s_val = s_key + SEG;  // insert only
-  uint16_t* s_lo = reinterpret_cast<uint16_t*>(s_val + (INS ? SEG : 0));
-  uint16_t* s_q0 = s_lo + SEG;  // two round queues, SEG entries each: i << 5 | o
-  __shared__ DeferBuf<INS, DBUF> B;
+  uint32_t* s_pos = s_val + (INS ? SEG : 0);  // round 2 only
+  uint16_t* s_lo = reinterpret_cast<uint16_t*>(s_pos + (R2 ? SEG : 0));
+  uint16_t* s_q0 = s_lo + SEG;  // keys open after round 0: i << 5 | o
+  __shared__ DeferBuf<INS, DBUF> B;   // -> DB
+  __shared__ DeferBuf<INS, DBUF> BA;  // -> DA
   __shared__ uint32_t s_qn[2];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int dirty;
@@ -484,6 +527,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
   if (threadIdx.x == 0) {
     dirty = 0;
     B.n = 0;
+    BA.n = 0;
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, (len + HALO) * 8u);
     bulk_load(tile, slots + rbase, len * 8u, &bar);
@@ -498,41 +542,44 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
   long long ops = 0, att = 0, win = 0, occ = 0, ndef = 0;
   bool claimed_any = false, waited = false;
 
-  // one probe step of segment key i from in-window offset o; returns true (and the
-  // queue entry) when the key stays open for the next round
-  auto step = [&](uint64_t s0, uint32_t i, uint32_t o, uint16_t* pe) -> bool {
+  // Sentinel test: with the default sentinels (t = e - 1) "free" is one subtract
+  // and compare, (c - t) <= 1.
+  const bool adj = t + 1u == e;
+  // one probe step of segment key i from in-window offset o (updated); returns true
+  // when the key stays open (nothing decisive in these slots, or a lost claim)
+  auto step = [&](uint64_t s0, uint32_t i, uint32_t& o) -> bool {
     const uint32_t k = s_key[i], lo = s_lo[i];
+    const uint32_t ri = R2 ? s_pos[i] : (uint32_t)(s0 + i);  // where the key's result goes
     uint64_t w[STEP];
 #pragma unroll
     for (int u = 0; u < (int)STEP; ++u) w[u] = INS ? lds64(tile + lo + o + u) : tile[lo + o + u];
-    uint32_t dec = 0;
+    // first decisive slot, scanning backwards with selects (no mask building)
+    const uint32_t room = WINDOW - o;  // slots left in the window
+    uint32_t u = STEP;
 #pragma unroll
-    for (int u = 0; u < (int)STEP; ++u) {
-      const uint32_t c = (uint32_t)w[u];
-      const bool d = INS ? ((c == k) | (c == e) | (c == t)) : ((c == k) | (c == e));  // lookups pass tombstones
-      dec |= (uint32_t)d << u;
+    for (int v = (int)STEP - 1; v >= 0; --v) {
+      const uint32_t c = (uint32_t)w[v];
+      bool d;
+      if (INS) d = (c == k) | (adj ? (c - t) <= 1u : ((c == e) | (c == t)));
+      else d = (c == k) | (c == e);  // lookups pass tombstones
+      u = (d && (uint32_t)v < room) ? (uint32_t)v : u;
     }
-    const uint32_t room = WINDOW - o;
-    if (room < STEP) dec &= (1u << room) - 1u;
-    if (!dec) {
+    if (u == STEP) {
       o += STEP;
-      if (o < WINDOW) {
-        *pe = (uint16_t)(i << 5 | o);
-        return true;
-      }
-      // window 0 holds neither the key nor a free cell: resume at window 1
-      defer_push(B, D, k, INS ? s_val[i] : 0u, (uint32_t)(s0 + i), WINDOW);
+      if (o < WINDOW) return true;
+      // the window holds neither the key nor a free cell: resume at the next one
+      defer_push(B, DB, k, INS ? s_val[i] : 0u, ri, OW + WINDOW);
       ndef += 1;
       return false;
     }
-    o += (uint32_t)__ffs(dec) - 1u;
+    o += u;
     const uint64_t wd = INS ? lds64(tile + lo + o) : tile[lo + o];
     const uint32_t c = (uint32_t)wd;
     if (INS) {
       if (c == k) {  // present before the first free cell (single_table.py:198-200)
-        status[s0 + i] = ST_DUPLICATE;
+        status[ri] = ST_DUPLICATE;
       } else if (c == t) {  // tombstone first: the deferred-claim rule (:201-223), COPS kernel
-        defer_push(B, D, k, s_val[i], (uint32_t)(s0 + i), 0);
+        defer_push(BA, DA, k, s_val[i], ri, OW);
         ndef += 1;
         return false;
       } else {
@@ -541,23 +588,22 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
           const unsigned long long want = ((unsigned long long)s_val[i] << 32) | k;
           won = atomicCAS((unsigned long long*)(tile + lo + o), (unsigned long long)wd, want) == wd;
         }
-        if (!won) {  // another key of this round took it: re-read it next round (:232-233)
+        if (!won) {  // another key took it: re-read from this slot (single_table.py:232-233)
           att += ug;
-          *pe = (uint16_t)(i << 5 | o);
           return true;
         }
         occ += 1;
         claimed_any = true;
-        status[s0 + i] = ST_INSERTED;
+        status[ri] = ST_INSERTED;
       }
     } else {
       const bool hit = c == k;
-      res_val[s0 + i] = hit ? (uint32_t)(wd >> 32) : 0u;
-      res_flag[s0 + i] = (uint8_t)hit;
+      res_val[ri] = hit ? (uint32_t)(wd >> 32) : 0u;
+      res_flag[ri] = (uint8_t)hit;
     }
     ops += 1;
-    att += (long long)chunk_end(o, ug);
-    win += 1;
+    att += (long long)(OW + chunk_end(o, ug));
+    win += R2 ? 2 : 1;
     return false;
   };
 
@@ -569,7 +615,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
     }
     // stage the segment (all loads in flight): keys, window starts (+ values)
     constexpr int PER = SEG / RT;
-    uint32_t kk[PER], vv[PER];
+    uint32_t kk[PER], vv[PER], pp[PER];
     uint16_t ll[PER];
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
@@ -577,6 +623,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
       kk[r] = i < m ? __ldcs(keys + s0 + i) : e;
       ll[r] = i < m ? __ldcs(los + s0 + i) : (uint16_t)0;
       if (INS) vv[r] = i < m ? __ldcs(vals + s0 + i) : 0u;
+      if (R2) pp[r] = i < m ? __ldcs(pos + s0 + i) : 0u;
     }
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
@@ -584,6 +631,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
       s_key[i] = kk[r];
       s_lo[i] = ll[r];
       if (INS) s_val[i] = vv[r];
+      if (R2) s_pos[i] = pp[r];
     }
     if (!waited) {
       mbar_wait(&bar, 0);
@@ -605,38 +653,32 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
             res_flag[s0 + i] = 0;
             ops += 1;  // retrieve_bulk counts every query (:403)
           }
-        } else if (INS && s_lo[i] + WINDOW > len) {  // window 0 leaves the staged region
-          defer_push(B, D, k, s_val[i], (uint32_t)(s0 + i), 0);
+        } else if (INS && s_lo[i] + WINDOW > len) {  // the window leaves the staged region
+          defer_push(BA, DA, k, s_val[i], R2 ? s_pos[i] : (uint32_t)(s0 + i), OW);
           ndef += 1;
         } else {
-          push = step(s0, i, 0, &pe);
+          uint32_t o = 0;
+          push = step(s0, i, o);
+          pe = (uint16_t)(i << 5 | o);
         }
       }
       queue_push(push, pe, s_q0, &s_qn[0]);
     }
-    // later rounds over the compacted queue
-    uint32_t cur = 0;
+    // the keys still open after round 0: every thread takes one from the queue and
+    // finishes it, step by step, then takes the next (no barrier between steps)
+    __syncthreads();
+    const uint32_t qn = s_qn[0];
     for (;;) {
-      __syncthreads();
-      const uint32_t qn = s_qn[cur];
-      if (qn == 0) break;
-      const uint32_t nxt = cur ^ 1u;
-      if (threadIdx.x == 0) s_qn[nxt] = 0;  // nobody pushes to nxt before the barrier below
-      __syncthreads();
-      const uint16_t* qc = s_q0 + cur * SEG;
-      for (uint32_t base = 0; base < qn; base += RT) {
-        const uint32_t j = base + threadIdx.x;
-        bool push = false;
-        uint16_t pe = 0;
-        if (j < qn) {
-          const uint32_t ent = qc[j];
-          push = step(s0, ent >> 5, ent & 31u, &pe);
-        }
-        queue_push(push, pe, s_q0 + nxt * SEG, &s_qn[nxt]);
+      const uint32_t j = atomicAdd(&s_qn[1], 1u);
+      if (j >= qn) break;
+      const uint32_t ent = s_q0[j];
+      const uint32_t i = ent >> 5;
+      uint32_t o = ent & 31u;
+      while (step(s0, i, o)) {
       }
-      cur = nxt;
     }
-    defer_flush(B, D, s0 + SEG >= k1);  // syncs: the segment buffers are free again
+    defer_flush(B, DB, s0 + SEG >= k1);  // syncs: the segment buffers are free again
+    defer_flush(BA, DA, s0 + SEG >= k1);
   }
   if (INS) {
     if (claimed_any) dirty = 1;
@@ -650,9 +692,10 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
   cta_add<6>(v, dst);
 }
 
-template <int MODE>
+template <int MODE, bool R2>
 constexpr size_t probe_smem() {
-  return (size_t)(ST_R + (MODE == 0 ? 0 : ST_HALO) + TILE_PAD) * 8 + (size_t)SEG * (4 + (MODE == 0 ? 4 : 0) + 2 + 4);
+  return (size_t)(ST_R + (MODE == 0 ? 0 : ST_HALO) + TILE_PAD) * 8 +
+         (size_t)SEG * (4 + (MODE == 0 ? 4 : 0) + (R2 ? 4 : 0) + 2 + 2);
 }
 
 // ------------------------------------------------------------- host side
@@ -678,19 +721,6 @@ bool staged_supported(const TableRef& T, uint64_t n) {
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // Scratch carving (one cudaMallocAsync per call, stream-ordered pool).
-struct StBufs {
-  uint32_t *gcount, *cur1, *cur2, *tstart;
-  uint64_t* foff;
-  void* scan;
-  size_t scan_bytes;
-  unsigned long long* dcount;
-  uint16_t *th1, *th2;
-  uint32_t *tg1, *tg2;
-  uint32_t *k1, *v1, *k2, *v2, *dx, *rv, *rv1;  // element arrays (u32)
-  uint16_t *inv1, *inv2, *lo2;                  // (u16)
-  uint8_t *rf, *rf1, *dO;                       // (u8)
-};
-
 struct Carver {
   char* q;
   size_t used = 0;
@@ -701,41 +731,97 @@ struct Carver {
   }
 };
 
-static StBufs st_carve(const StPlan& p, uint64_t n, bool vals, void* base, size_t* total) {
+// One forward round: histogram + scan + plan + one or two tile partitions.
+struct Round {
+  uint32_t *gcount, *cur1, *cur2, *tstart;
+  uint64_t* foff;
+  void* scan;
+  size_t scan_bytes;
+  uint32_t *k1, *v1, *p1, *r1, *k2, *v2, *p2;  // level-1 / level-2 outputs (payloads v, p, r)
+  uint16_t* lo2;
+  uint16_t *inv1, *inv2, *th1, *th2;  // inverse (round 1 only)
+  uint32_t *tg1, *tg2;
+};
+
+struct StBufs {
+  Round r1, r2, rd;                // round 1, round 2 (optional), deferred-key ordering (level 1 only)
+  unsigned long long* dcount;     // [0]: list A (COPS kernels), [1]: list B (round 2)
+  uint32_t *ak, *av, *ax, *ao, *bk, *bv, *bx, *bo;
+  uint32_t *rv, *rv1;  // lookup: values in region order / level-1 order
+  uint8_t *rf, *rf1;   // lookup: found flags; insert: statuses
+};
+
+static void carve_round(Carver& c, Round& r, const StPlan& p, uint64_t n, int npay, bool inverse, int levels) {
+  r = Round{};
+  r.gcount = (uint32_t*)c.take(p.regions * 4ull);
+  r.foff = (uint64_t*)c.take((p.regions + 1ull) * 8);
+  r.scan_bytes = align_up(exclusive_scan_scratch_bytes(p.regions));
+  r.scan = c.take(r.scan_bytes);
+  r.cur1 = (uint32_t*)c.take(PBINS * 4ull);
+  r.cur2 = (uint32_t*)c.take(p.regions * 4ull);
+  r.tstart = (uint32_t*)c.take((p.supers + 1ull) * 4);
+  r.k1 = (uint32_t*)c.take(n * 4);
+  r.v1 = npay >= 1 ? (uint32_t*)c.take(n * 4) : nullptr;
+  r.p1 = npay >= 2 ? (uint32_t*)c.take(n * 4) : nullptr;
+  r.r1 = npay >= 3 ? (uint32_t*)c.take(n * 4) : nullptr;
+  if (levels == 2) {
+    r.k2 = (uint32_t*)c.take(n * 4);
+    r.v2 = npay >= 1 ? (uint32_t*)c.take(n * 4) : nullptr;
+    r.p2 = npay >= 2 ? (uint32_t*)c.take(n * 4) : nullptr;
+    r.lo2 = (uint16_t*)c.take(n * 2);
+  }
+  if (inverse) {
+    r.inv1 = (uint16_t*)c.take(n * 2);
+    r.inv2 = (uint16_t*)c.take(n * 2);
+    r.th1 = (uint16_t*)c.take(p.tiles1 * p.supers * 2);
+    r.tg1 = (uint32_t*)c.take(p.tiles1 * p.supers * 4);
+    r.th2 = (uint16_t*)c.take(p.tiles2 * 256 * 2);
+    r.tg2 = (uint32_t*)c.take(p.tiles2 * 256 * 4);
+  }
+}
+
+static StBufs st_carve(const StPlan& p, uint64_t n, bool ins, bool round2, void* base, size_t* total) {
   Carver c{static_cast<char*>(base)};
   StBufs b;
-  b.gcount = (uint32_t*)c.take(p.regions * 4ull);
-  b.foff = (uint64_t*)c.take((p.regions + 1ull) * 8);
-  b.scan_bytes = align_up(exclusive_scan_scratch_bytes(p.regions));
-  b.scan = c.take(b.scan_bytes);
-  b.cur1 = (uint32_t*)c.take(PBINS * 4ull);
-  b.cur2 = (uint32_t*)c.take(p.regions * 4ull);
-  b.tstart = (uint32_t*)c.take((p.supers + 1ull) * 4);
+  carve_round(c, b.r1, p, n, ins ? 1 : 0, true, 2);
+  if (round2) carve_round(c, b.r2, p, n, ins ? 2 : 1, false, 2);
+  carve_round(c, b.rd, p, n, ins ? 3 : 2, false, 1);
   b.dcount = (unsigned long long*)c.take(64);
-  b.th1 = (uint16_t*)c.take(p.tiles1 * p.supers * 2);
-  b.tg1 = (uint32_t*)c.take(p.tiles1 * p.supers * 4);
-  b.th2 = (uint16_t*)c.take(p.tiles2 * 256 * 2);
-  b.tg2 = (uint32_t*)c.take(p.tiles2 * 256 * 4);
-  b.k1 = (uint32_t*)c.take(n * 4);  // later: deferred keys
-  b.v1 = vals ? (uint32_t*)c.take(n * 4) : nullptr;  // later: deferred values
-  b.k2 = (uint32_t*)c.take(n * 4);
-  b.v2 = vals ? (uint32_t*)c.take(n * 4) : nullptr;
-  b.dx = (uint32_t*)c.take(n * 4);
-  b.rv = vals ? nullptr : (uint32_t*)c.take(n * 4);
-  b.rv1 = vals ? nullptr : (uint32_t*)c.take(n * 4);
-  b.inv1 = (uint16_t*)c.take(n * 2);
-  b.inv2 = (uint16_t*)c.take(n * 2);
-  b.lo2 = (uint16_t*)c.take(n * 2);
-  b.rf = (uint8_t*)c.take(n);  // insert: status in region order
+  b.ak = (uint32_t*)c.take(n * 4);
+  b.av = ins ? (uint32_t*)c.take(n * 4) : nullptr;
+  b.ax = (uint32_t*)c.take(n * 4);
+  b.ao = (uint32_t*)c.take(n * 4);
+  b.bk = round2 ? (uint32_t*)c.take(n * 4) : b.ak;  // without round 2, one list
+  b.bv = round2 ? (ins ? (uint32_t*)c.take(n * 4) : nullptr) : b.av;
+  b.bx = round2 ? (uint32_t*)c.take(n * 4) : b.ax;
+  b.bo = round2 ? (uint32_t*)c.take(n * 4) : b.ao;
+  b.rv = ins ? nullptr : (uint32_t*)c.take(n * 4);
+  b.rv1 = ins ? nullptr : (uint32_t*)c.take(n * 4);
+  b.rf = (uint8_t*)c.take(n);
   b.rf1 = (uint8_t*)c.take(n);
-  b.dO = (uint8_t*)c.take(n);
   *total = c.used;
   return b;
 }
 
+// staged window-1 round for the deferred keys: off by default (CH_STAGED_ROUND2=1 enables it).
+// At load 0.95 ~40% of the round-2 keys defer again and the COPS kernel then walks windows
+// >= 2 for them, so the extra region pass did not pay (profiles/r01_staged_round2.txt).
+static bool g_round2 = [] {
+  const char* e = getenv("CH_STAGED_ROUND2");
+  return e && e[0] == '1';
+}();
+
+// CTAs per SM of the deferred-key COPS pass (CH_STAGED_FB_CTAS; default 0 = a full wave,
+// which measured fastest: 1 / 2 / full per SM -> 20.1 / 20.1 / 21.6 G ops/s).
+static int g_fb_blocks = [] {
+  const char* e = getenv("CH_STAGED_FB_CTAS");
+  const int v = e ? atoi(e) : 0;
+  return v > 0 ? v : 0;
+}();
+
 size_t staged_scratch_bytes(const TableRef& T, uint64_t n, bool insert) {
   size_t total = 0;
-  st_carve(st_plan(T, n), n, insert, nullptr, &total);
+  st_carve(st_plan(T, n), n, insert, g_round2, nullptr, &total);
   return total;
 }
 
@@ -746,15 +832,6 @@ static int st_smem(KS kern, size_t bytes) {
   if (!rc && bytes > (48u << 10))
     rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
   return rc;
-}
-
-// persistent grid: one wave of CTAs (no more than there are tiles)
-template <typename KS>
-static unsigned persist_grid(const Launch& lc, KS kern, size_t smem, uint64_t tiles) {
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT, smem) != cudaSuccess || occ < 1) occ = 1;
-  const uint64_t full = (uint64_t)lc.sms * occ;
-  return (unsigned)(tiles < full ? tiles : full);
 }
 
 static int st_timed(const Launch& lc, cudaEvent_t* e0) {
@@ -770,50 +847,38 @@ static void st_timed_end(const Launch& lc, cudaEvent_t e0) {
   }
 }
 
-// count + scan + plan + L1 + L2: keys (and values) in region order, window starts
-static int st_forward(const Launch& lc, const TableRef& T, const StPlan& p, const StBufs& b, const uint32_t* keys,
-                      const uint32_t* vals, uint64_t n) {
-  int rc = cuda_check(cudaMemsetAsync(b.gcount, 0, p.regions * 4ull, lc.stream), "memset");
-  if (!rc) rc = cuda_check(cudaMemsetAsync(b.dcount, 0, 8, lc.stream), "memset");
+// One forward round over keys k (+ payloads v, q, w): count + scan + plan + L1 (+ L2).
+// n_dev: the round's count lives on the device (n is the capacity).  wj: window.
+template <int NPAY>
+static int st_forward(const Launch& lc, const TableRef& T, const StPlan& p, const Round& r, const uint32_t* k,
+                      const uint32_t* v, const uint32_t* q, const uint32_t* w, uint64_t n,
+                      const unsigned long long* n_dev, int wj, int levels) {
+  int rc = cuda_check(cudaMemsetAsync(r.gcount, 0, p.regions * 4ull, lc.stream), "memset");
   if (rc) return rc;
   const size_t csmem = p.regions * 4ull;
   if ((rc = st_smem(k_st_count, csmem))) return rc;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_st_count, 1024, csmem);
   if (occ < 1) occ = 1;
-  k_st_count<<<(unsigned)(lc.sms * occ), 1024, csmem, lc.stream>>>(T, keys, n, p.regions, b.gcount);
+  k_st_count<<<(unsigned)(lc.sms * occ), 1024, csmem, lc.stream>>>(T, k, n, p.regions, r.gcount, n_dev, wj);
   count_launch();
   if ((rc = cuda_check(cudaGetLastError(), "staged count"))) return rc;
-  if ((rc = exclusive_scan_u32(lc, b.gcount, p.regions, b.foff, b.scan, b.scan_bytes))) return rc;
-  k_st_plan<<<1, PT, 0, lc.stream>>>(b.foff, p.regions, p.supers, b.cur1, b.cur2, b.tstart);
+  if ((rc = exclusive_scan_u32(lc, r.gcount, p.regions, r.foff, r.scan, r.scan_bytes))) return rc;
+  k_st_plan<<<1, PT, 0, lc.stream>>>(r.foff, p.regions, p.supers, r.cur1, r.cur2, r.tstart);
   count_launch();
-  const bool V = vals != nullptr;
-  // bucketed (k [, v], bucket, level 2: window start)
-  const size_t sm1 = (size_t)PTILE * (4 + (V ? 4 : 0) + 2), sm2 = sm1 + PTILE * 2;
+  // bucketed (k, payloads, bucket id, level 2: window start)
+  const size_t sm1 = (size_t)PTILE * (4 + 4 * NPAY + 2), sm2 = sm1 + PTILE * 2;
   const unsigned t1 = (unsigned)p.tiles1, t2 = (unsigned)p.tiles2;
-  if (V) {
-    auto k1f = k_st_split<1, true>;
-    auto k2f = k_st_split<2, true>;
-    if ((rc = st_smem(k1f, sm1)) || (rc = st_smem(k2f, sm2))) return rc;
-    k1f<<<t1, PT, sm1, lc.stream>>>(T, n, b.foff, b.tstart, p.supers, p.regions, t1, keys,
-                                                                 vals, b.k1, b.v1, nullptr, b.inv1, b.th1, b.tg1,
-                                                                 p.supers, b.cur1);
-    count_launch();
-    k2f<<<t2, PT, sm2, lc.stream>>>(T, n, b.foff, b.tstart, p.supers, p.regions, t2, b.k1,
-                                                                 b.v1, b.k2, b.v2, b.lo2, b.inv2, b.th2, b.tg2, 256,
-                                                                 b.cur2);
-    count_launch();
-  } else {
-    auto k1f = k_st_split<1, false>;
-    auto k2f = k_st_split<2, false>;
-    if ((rc = st_smem(k1f, sm1)) || (rc = st_smem(k2f, sm2))) return rc;
-    k1f<<<t1, PT, sm1, lc.stream>>>(T, n, b.foff, b.tstart, p.supers, p.regions, t1, keys,
-                                                                 nullptr, b.k1, nullptr, nullptr, b.inv1, b.th1,
-                                                                 b.tg1, p.supers, b.cur1);
-    count_launch();
-    k2f<<<t2, PT, sm2, lc.stream>>>(T, n, b.foff, b.tstart, p.supers, p.regions, t2, b.k1,
-                                                                 nullptr, b.k2, nullptr, b.lo2, b.inv2, b.th2, b.tg2,
-                                                                 256, b.cur2);
+  auto k1f = k_st_split<1, NPAY>;
+  if ((rc = st_smem(k1f, sm1))) return rc;
+  k1f<<<t1, PT, sm1, lc.stream>>>(T, n, r.foff, r.tstart, p.supers, p.regions, t1, k, v, q, w, r.k1, r.v1, r.p1, r.r1,
+                                   nullptr, r.inv1, r.th1, r.tg1, p.supers, r.cur1, n_dev, wj);
+  count_launch();
+  if (levels == 2) {
+    auto k2f = k_st_split<2, NPAY < 2 ? NPAY : 2>;
+    if ((rc = st_smem(k2f, sm2))) return rc;
+    k2f<<<t2, PT, sm2, lc.stream>>>(T, n, r.foff, r.tstart, p.supers, p.regions, t2, r.k1, r.v1, r.p1, nullptr, r.k2,
+                                     r.v2, r.p2, nullptr, r.lo2, r.inv2, r.th2, r.tg2, 256, r.cur2, n_dev, wj);
     count_launch();
   }
   return cuda_check(cudaGetLastError(), "staged partition");
@@ -823,41 +888,64 @@ static int st_forward(const Launch& lc, const TableRef& T, const StPlan& p, cons
 template <bool VAL>
 static int st_backward(const Launch& lc, const StPlan& p, const StBufs& b, uint64_t n, const uint32_t* rv,
                        const uint8_t* rf, uint32_t* out_v, uint8_t* out_f) {
+  const Round& r = b.r1;
   const unsigned t1 = (unsigned)p.tiles1, t2 = (unsigned)p.tiles2;
   auto g2 = k_st_gather<2, VAL>;
   auto g1 = k_st_gather<1, VAL>;
-  g2<<<t2, PT, 0, lc.stream>>>(n, b.foff, b.tstart, p.supers, p.regions, t2, b.inv2, b.th2,
-                                                         b.tg2, 256, rv, rf, b.rv1, b.rf1);
+  g2<<<t2, PT, 0, lc.stream>>>(n, r.foff, r.tstart, p.supers, p.regions, t2, r.inv2, r.th2, r.tg2, 256, rv, rf, b.rv1,
+                                b.rf1);
   count_launch();
-  g1<<<t1, PT, 0, lc.stream>>>(n, b.foff, b.tstart, p.supers, p.regions, t1, b.inv1, b.th1,
-                                                         b.tg1, p.supers, b.rv1, b.rf1, out_v, out_f);
+  g1<<<t1, PT, 0, lc.stream>>>(n, r.foff, r.tstart, p.supers, p.regions, t1, r.inv1, r.th1, r.tg1, p.supers, b.rv1,
+                                b.rf1, out_v, out_f);
   count_launch();
   return cuda_check(cudaGetLastError(), "staged gather");
+}
+
+template <int MODE, bool R2>
+static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const Round& r, const uint32_t* pos,
+                    uint8_t* status, uint32_t* rv, uint8_t* rf, const DeferOut& DA, const DeferOut& DB, int g) {
+  const size_t sm = probe_smem<MODE, R2>();
+  auto kern = k_st_probe<MODE, R2>;
+  int rc = st_smem(kern, sm);
+  if (rc) return rc;
+  cudaEvent_t e0;
+  if (!R2) st_timed(lc, &e0);  // the dominant kernel of the staged schedule (bench.py roofline)
+  kern<<<p.regions, RT, sm, lc.stream>>>(T, r.foff, r.k2, MODE == 0 ? r.v2 : nullptr, pos, r.lo2, status, rv, rf, DA,
+                                         DB, g);
+  count_launch();
+  if (!R2) st_timed_end(lc, e0);
+  return cuda_check(cudaGetLastError(), "staged region probe");
 }
 
 int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, const void* vals,
                   uint64_t n, uint8_t* status, void* scratch) {
   const StPlan p = st_plan(T, n);
   size_t total = 0;
-  const StBufs b = st_carve(p, n, true, scratch, &total);
-  int rc = st_forward(lc, T, p, b, (const uint32_t*)keys, (const uint32_t*)vals, n);
+  const bool r2 = g_round2;
+  const StBufs b = st_carve(p, n, true, r2, scratch, &total);
+  int rc = cuda_check(cudaMemsetAsync(b.dcount, 0, 16, lc.stream), "memset");
+  if (!rc)
+    rc = st_forward<1>(lc, T, p, b.r1, (const uint32_t*)keys, (const uint32_t*)vals, nullptr, nullptr, n, nullptr, 0,
+                       2);
   if (rc) return rc;
-  const size_t sm = probe_smem<0>();
-  if ((rc = st_smem(k_st_probe<0>, sm))) return rc;
-  cudaEvent_t e0;
-  st_timed(lc, &e0);
-  const DeferOut D{b.k1, b.v1, b.dx, b.dO, b.dcount};  // the deferred list reuses the L1 arrays
-  k_st_probe<0><<<p.regions, RT, sm, lc.stream>>>(T, b.foff, b.k2, b.v2, b.lo2, b.rf, nullptr, nullptr, D, ts.g);
-  count_launch();
-  st_timed_end(lc, e0);
-  if ((rc = cuda_check(cudaGetLastError(), "staged region insert"))) return rc;
-  Launch rest = lc;  // deferred keys: COPS kernels, statuses at their region-ordered positions
+  const DeferOut DA{b.ak, b.av, b.ax, b.ao, b.dcount};
+  const DeferOut DB{b.bk, b.bv, b.bx, b.bo, r2 ? b.dcount + 1 : b.dcount};
+  if ((rc = st_probe<0, false>(lc, T, p, b.r1, nullptr, b.rf, nullptr, nullptr, DA, DB, ts.g))) return rc;
+  if (r2) {  // window 1 of the keys whose window 0 was full, staged the same way
+    if ((rc = st_forward<2>(lc, T, p, b.r2, b.bk, b.bv, b.bx, nullptr, n, b.dcount + 1, 1, 2))) return rc;
+    if ((rc = st_probe<0, true>(lc, T, p, b.r2, b.r2.p2, b.rf, nullptr, nullptr, DA, DA, ts.g))) return rc;
+  }
+  // the rest: COPS kernels over the deferred keys ordered by their window-1 super-region
+  // (consecutive CTAs probe one L2-resident stretch of the table), statuses to their
+  // region-ordered positions
+  if ((rc = st_forward<3>(lc, T, p, b.rd, b.ak, b.av, b.ax, b.ao, n, b.dcount, 1, 1))) return rc;
+  Launch rest = lc;
   rest.timer = nullptr;
   rest.n_dev = b.dcount;
-  rest.out_idx = b.dx;
-  rest.o_start = b.dO;
-  if ((rc = single_insert(rest, T, ts, b.k1, b.v1, n, b.rf, nullptr, 0))) return rc;
-  // statuses back to the caller's order (u8 only)
+  rest.out_idx = b.rd.p1;
+  rest.o_start = b.rd.r1;
+  rest.max_blocks = g_fb_blocks * lc.sms;
+  if ((rc = single_insert(rest, T, ts, b.rd.k1, b.rd.v1, n, b.rf, nullptr, 0))) return rc;
   return st_backward<false>(lc, p, b, n, nullptr, b.rf, nullptr, status);
 }
 
@@ -865,24 +953,27 @@ int staged_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
                   void* vals_out, uint8_t* found, void* scratch) {
   const StPlan p = st_plan(T, n);
   size_t total = 0;
-  const StBufs b = st_carve(p, n, false, scratch, &total);
-  int rc = st_forward(lc, T, p, b, (const uint32_t*)keys, nullptr, n);
+  const bool r2 = g_round2;
+  const StBufs b = st_carve(p, n, false, r2, scratch, &total);
+  int rc = cuda_check(cudaMemsetAsync(b.dcount, 0, 16, lc.stream), "memset");
+  if (!rc) rc = st_forward<0>(lc, T, p, b.r1, (const uint32_t*)keys, nullptr, nullptr, nullptr, n, nullptr, 0, 2);
   if (rc) return rc;
-  const size_t sm = probe_smem<1>();
-  if ((rc = st_smem(k_st_probe<1>, sm))) return rc;
-  cudaEvent_t e0;
-  st_timed(lc, &e0);
-  const DeferOut D{b.k1, nullptr, b.dx, b.dO, b.dcount};
-  k_st_probe<1><<<p.regions, RT, sm, lc.stream>>>(T, b.foff, b.k2, nullptr, b.lo2, nullptr, b.rv, b.rf, D, ts.g);
-  count_launch();
-  st_timed_end(lc, e0);
-  if ((rc = cuda_check(cudaGetLastError(), "staged region lookup"))) return rc;
+  const DeferOut DA{b.ak, nullptr, b.ax, b.ao, b.dcount};
+  const DeferOut DB{b.bk, nullptr, b.bx, b.bo, r2 ? b.dcount + 1 : b.dcount};
+  if ((rc = st_probe<1, false>(lc, T, p, b.r1, nullptr, nullptr, b.rv, b.rf, DA, DB, ts.g))) return rc;
+  if (r2) {  // window 1 of the keys whose window 0 decided nothing (positions ride as the payload)
+    if ((rc = st_forward<1>(lc, T, p, b.r2, b.bk, b.bx, nullptr, nullptr, n, b.dcount + 1, 1, 2))) return rc;
+    if ((rc = st_probe<1, true>(lc, T, p, b.r2, b.r2.v2, nullptr, b.rv, b.rf, DA, DA, ts.g))) return rc;
+  }
+  // deferred keys ordered by window-1 super-region (payloads: position, resume offset)
+  if ((rc = st_forward<2>(lc, T, p, b.rd, b.ak, b.ax, b.ao, nullptr, n, b.dcount, 1, 1))) return rc;
   Launch rest = lc;
   rest.timer = nullptr;
   rest.n_dev = b.dcount;
-  rest.out_idx = b.dx;
-  rest.o_start = b.dO;
-  if ((rc = single_lookup(rest, T, ts, b.k1, n, b.rv, b.rf, nullptr, nullptr, nullptr, 0))) return rc;
+  rest.out_idx = b.rd.v1;
+  rest.o_start = b.rd.p1;
+  rest.max_blocks = g_fb_blocks * lc.sms;
+  if ((rc = single_lookup(rest, T, ts, b.rd.k1, n, b.rv, b.rf, nullptr, nullptr, nullptr, 0))) return rc;
   return st_backward<true>(lc, p, b, n, b.rv, b.rf, (uint32_t*)vals_out, found);
 }
 

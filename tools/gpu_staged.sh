@@ -7,4 +7,4 @@ timeout 300 python bench.py --no-cpu ${LOC:+--locality $LOC} > gpurun_out/bench.
 cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:"k_|tile" --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu ${LOC:+--locality $LOC} > /dev/null 2>&1
-python tools/launches.py gpurun_out/launches.csv | tail -40
+python tools/launches.py gpurun_out/launches.csv 60 | grep -v "k_tile\|k_zero\|k_reset\|k_st_plan" | tail -30
