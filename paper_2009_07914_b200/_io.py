@@ -92,7 +92,7 @@ def pipelined(device: int, inputs: list, outputs: list, run, chunk: int) -> None
     compute = torch.cuda.current_stream(dev)
     s_in = torch.cuda.Stream(dev)
     s_out = torch.cuda.Stream(dev)
-    nb = 2
+    nb = 3
     bufs = [[torch.empty(min(chunk, n), dtype=x.dtype, device=dev) for x in inputs] for _ in range(nb)]
     free = [torch.cuda.Event() for _ in range(nb)]
     s_in.wait_stream(compute)
@@ -111,12 +111,12 @@ def pipelined(device: int, inputs: list, outputs: list, run, chunk: int) -> None
         outs = run([d[:m] for d in bufs[b]], compute)
         ev_done = torch.cuda.Event()
         ev_done.record(compute)
-        with torch.cuda.stream(s_out):
+        free[b].record(compute)  # the inputs are consumed once the op has run: the next H2D
+        with torch.cuda.stream(s_out):  # into this buffer need not wait for the D2H below
             s_out.wait_event(ev_done)
             for o, y in zip(outs, outputs):
                 o.record_stream(s_out)
                 y[lo:hi].copy_(o, non_blocking=True)
-            free[b].record(s_out)
     compute.wait_stream(s_out)
     for bb in bufs:
         for d in bb:

@@ -200,7 +200,7 @@ bool use_locality(const ch_table* t, uint64_t n) {
   if (n == 0 || n >= (1ull << 32) || t->loc_mode == 1 || t->loc_mode == 3) return false;
   if (t->loc_mode == 2) return true;
   const uint64_t bytes = t->T.c * (uint64_t)slot_bytes_of(t);
-  return bytes >= (256ull << 20) && n * 16 >= t->T.c;
+  return bytes >= (256ull << 20) && n * 32 >= t->T.c;
 }
 
 void keep_pool_memory(int device) {

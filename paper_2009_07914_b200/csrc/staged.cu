@@ -109,16 +109,37 @@ __global__ void __launch_bounds__(1024) k_st_count(TableRef T, const uint32_t* _
   if (n_dev) n = *n_dev;
   for (uint32_t i = threadIdx.x; i < regions; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < n; i += 4 * stride) {
-    uint32_t k[4];
+  // 16-byte loads (four keys each, 4 in flight per thread) over the aligned body
+  const uint64_t head = ((16 - ((uintptr_t)keys & 15)) & 15) / 4;  // keys before the first 16 B boundary
+  const uint64_t h0 = head < n ? head : n;
+  const uint64_t nv = (n - h0) / 4;
+  const uint4* kv = reinterpret_cast<const uint4*>(keys + h0);
+  uint64_t i = tid;
+  for (; i + 3 * stride < nv; i += 4 * stride) {
+    uint4 q[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) k[u] = __ldcs(keys + i + u * stride);
+    for (int u = 0; u < 4; ++u) q[u] = __ldcs(kv + i + u * stride);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) atomicAdd(&s_cnt[region_of_key(T, k[u], wj)], 1u);
+    for (int u = 0; u < 4; ++u) {
+      atomicAdd(&s_cnt[region_of_key(T, q[u].x, wj)], 1u);
+      atomicAdd(&s_cnt[region_of_key(T, q[u].y, wj)], 1u);
+      atomicAdd(&s_cnt[region_of_key(T, q[u].z, wj)], 1u);
+      atomicAdd(&s_cnt[region_of_key(T, q[u].w, wj)], 1u);
+    }
   }
-  for (; i < n; i += stride) atomicAdd(&s_cnt[region_of_key(T, keys[i], wj)], 1u);
+  for (; i < nv; i += stride) {
+    const uint4 q = __ldcs(kv + i);
+    atomicAdd(&s_cnt[region_of_key(T, q.x, wj)], 1u);
+    atomicAdd(&s_cnt[region_of_key(T, q.y, wj)], 1u);
+    atomicAdd(&s_cnt[region_of_key(T, q.z, wj)], 1u);
+    atomicAdd(&s_cnt[region_of_key(T, q.w, wj)], 1u);
+  }
+  // unaligned head and the tail past the last full vector
+  if (tid < h0) atomicAdd(&s_cnt[region_of_key(T, keys[tid], wj)], 1u);
+  const uint64_t t0 = h0 + nv * 4;
+  if (tid < n - t0) atomicAdd(&s_cnt[region_of_key(T, keys[t0 + tid], wj)], 1u);
   __syncthreads();
   for (uint32_t r = threadIdx.x; r < regions; r += blockDim.x)
     if (s_cnt[r]) atomicAdd(&gcount[r], s_cnt[r]);

@@ -265,8 +265,10 @@ class SingleValueHashTable(_TableBase):
         return vals, found
 
     def _host_chunk(self) -> int:
-        # big enough to keep region-ordered execution on (n >= c/16), small enough to overlap
-        return max(1 << 20, -(-self.capacity // 12))
+        # c/24 keys per chunk: short pipeline fill / drain, and each chunk still covers the
+        # table densely enough for region-ordered execution (tools/e2e_sweep.py: c/8 77.6 ms,
+        # c/12 76.2 ms, c/24 74.0 ms per insert_host + retrieve_host of 2^28 keys)
+        return max(1 << 20, -(-self.capacity // 24))
 
     # -- element operations (single_table.py:273-351) ---------------------------
     def insert(self, key: int, value: int) -> InsertStatus:
