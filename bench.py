@@ -382,13 +382,21 @@ def main() -> None:
         ins_gops = n * world / (ins_ms_max * 1e-3) / 1e9
         ret_gops = n * world / (ret_ms_max * 1e-3) / 1e9
         # dominant kernel: the longer of the insert / retrieve probe kernels, timed with
-        # CUDA events inside the library on the stream they run on (one launch each per step)
-        if k_ins_ms >= k_ret_ms:
-            kname, kms, kbytes = "k_insert", k_ins_ms, INSERT_BYTES
+        # CUDA events inside the library on the stream they run on (one launch each per op).
+        # Algorithmic bytes per launch: staged region passes stream the table
+        # (read + write back for insert) and 11 B per key (key, value, window start, status /
+        # value + found); direct probes touch one 32 B sector per key.
+        sched_name = table.batch_schedule(n)
+        c = table.capacity
+        if sched_name == "staged":
+            cand = [("k_st_probe<0> (staged insert)", k_ins_ms, 16 * c + 11 * n),
+                    ("k_st_probe<1> (staged retrieve)", k_ret_ms, 8 * c + 11 * n)]
         else:
-            kname, kms, kbytes = "k_lookup", k_ret_ms, RETRIEVE_BYTES
-        keys_per_launch = n if world == 1 else n  # weak scaling: ~n keys per rank and launch
-        achieved = kbytes * keys_per_launch / (kms * 1e-3) / 1e9
+            cand = [("k_insert", k_ins_ms, INSERT_BYTES * n), ("k_lookup", k_ret_ms, RETRIEVE_BYTES * n)]
+        kname, kms, kbytes_launch = max(cand, key=lambda x: x[1])
+        keys_per_launch = n  # weak scaling: ~n keys per rank and launch
+        achieved = kbytes_launch / (kms * 1e-3) / 1e9
+        kbytes = kbytes_launch / keys_per_launch
         tr = ncu_traffic().get(kname) if world == 1 else None
         traffic = tr.get("dram_bytes") if isinstance(tr, dict) else tr
         cpu = None
@@ -410,10 +418,12 @@ def main() -> None:
                        "l2": "inputs (2 GiB) and table (2.1 GiB) exceed the 126 MB L2; no flush"},
             "insert_gops": ins_gops, "retrieve_gops": ret_gops,
             "phase_ms": {"clear": clear_ms, "insert": ins_ms, "retrieve": ret_ms,
-                         "k_insert": k_ins_ms, "k_lookup": k_ret_ms},
+                         "probe_insert": k_ins_ms, "probe_retrieve": k_ret_ms},
+            "schedule_kind": sched_name,
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "bytes_per_op": kbytes, "ops_per_launch": keys_per_launch, "traffic": traffic,
+                         "bytes_per_op": kbytes, "bytes_per_launch": kbytes_launch,
+                         "ops_per_launch": keys_per_launch, "traffic": traffic,
                          "kernel_ms": kms},
             "schedule": sched,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks.summary(),

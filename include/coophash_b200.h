@@ -92,6 +92,9 @@ int ch_synchronize(ch_table* t);
  * order (csrc/locality.cu), 3 shared-memory staged regions (csrc/staged.cu; packed only, other
  * layouts run direct).  Result semantics are identical; only the schedule changes. */
 int ch_set_locality(ch_table* t, int mode);
+/* the schedule a single-value bulk insert / retrieve of n keys takes: 1 direct probes,
+ * 2 L2 region order, 3 shared-memory staged regions (bench.py reports it) */
+int ch_batch_schedule(ch_table* t, uint64_t n);
 /* CUDA-event timing of the table's probe kernels (insert / lookup / multi passes):
  * enable, then read each launch's device time in launch order (up to cap entries) and
  * the number of launches timed (synchronizes, resets) */

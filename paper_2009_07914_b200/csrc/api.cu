@@ -449,6 +449,14 @@ int ch_set_locality(ch_table* t, int mode) {
   return CH_OK;
 }
 
+int ch_batch_schedule(ch_table* t, uint64_t n) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  std::lock_guard<std::mutex> lock(t->mu);
+  if (t->cfg.kind != CH_SINGLE) return 1;
+  if (use_staged(t, n)) return 3;
+  return use_locality(t, n) ? 2 : 1;
+}
+
 int ch_synchronize(ch_table* t) {
   if (!t) return fail(CH_EINVAL, "null table");
   DeviceGuard dev(t->cfg.device);

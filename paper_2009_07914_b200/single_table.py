@@ -135,6 +135,13 @@ class _TableBase:
         code = {"auto": 0, "off": 1, "on": 2, "staged": 3}.get(mode, mode)
         _lib.check(_lib.lib().ch_set_locality(self._dt.handle, int(code)), "set_locality")
 
+    def batch_schedule(self, n: int) -> str:
+        """Schedule a bulk insert / retrieve of n keys takes: "direct", "l2_order" or "staged"."""
+        code = _lib.lib().ch_batch_schedule(self._dt.handle, int(n))
+        if code < 0:
+            _lib.check(code, "batch_schedule")
+        return {1: "direct", 2: "l2_order", 3: "staged"}[code]
+
     def kernel_timing(self, enable: bool = True) -> None:
         """Record CUDA events around every probe-kernel launch of this table."""
         _lib.check(_lib.lib().ch_kernel_timing(self._dt.handle, int(bool(enable))), "kernel_timing")
