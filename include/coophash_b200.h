@@ -95,6 +95,9 @@ int ch_set_locality(ch_table* t, int mode);
 /* the schedule a single-value bulk insert / retrieve of n keys takes: 1 direct probes,
  * 2 L2 region order, 3 shared-memory staged regions (bench.py reports it) */
 int ch_batch_schedule(ch_table* t, uint64_t n);
+/* multi-value bulk insert: 1 (default) groups the batch by key and walks each distinct key's
+ * sequence once (csrc/mgroup.cu, batches >= 4096 pairs); 0 inserts pair by pair */
+int ch_set_multi_grouping(ch_table* t, int on);
 /* CUDA-event timing of the table's probe kernels (insert / lookup / multi passes):
  * enable, then read each launch's device time in launch order (up to cap entries) and
  * the number of launches timed (synchronizes, resets) */

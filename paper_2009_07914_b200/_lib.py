@@ -51,6 +51,7 @@ _SIGS = {
     "ch_synchronize": (C.c_int, [_P]),
     "ch_set_locality": (C.c_int, [_P, C.c_int]),
     "ch_batch_schedule": (C.c_int, [_P, _U64]),
+    "ch_set_multi_grouping": (C.c_int, [_P, C.c_int]),
     "ch_kernel_timing": (C.c_int, [_P, C.c_int]),
     "ch_kernel_time": (C.c_int, [_P, C.POINTER(C.c_double), C.c_uint64, C.POINTER(C.c_uint64)]),
     "ch_insert": (C.c_int, [_P, _P, _P, _U64, _P, _P]),

@@ -57,6 +57,9 @@ int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
                   uint64_t n, uint8_t* status, void* scratch);
 int staged_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
                   void* vals_out, uint8_t* found, void* scratch);
+size_t mgroup_scratch_bytes(uint64_t n, int kbytes, int vbytes);
+int multi_insert_grouped(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, const void* vals,
+                         uint64_t n, uint8_t* status, void* scratch, size_t scratch_bytes);
 int bucket_walk(const Launch& lc, const BucketRef& B, int vbytes, const uint64_t* handles, uint64_t n,
                 const uint64_t* offsets, void* out);
 
@@ -86,6 +89,7 @@ struct ch_table {
   // big-batch schedule: 0 auto, 1 direct, 2 L2 region order (locality.cu),
   // 3 shared-memory staged regions (staged.cu, packed 32|32 tables)
   int loc_mode = 0;
+  int group_mode = 0;  // multi-value bulk insert: 0 grouped for n >= 4096, 1 per pair
   bool timing = false;
   KernelTimer timer;
 };
@@ -449,6 +453,13 @@ int ch_set_locality(ch_table* t, int mode) {
   return CH_OK;
 }
 
+int ch_set_multi_grouping(ch_table* t, int on) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  std::lock_guard<std::mutex> lock(t->mu);
+  t->group_mode = on ? 0 : 1;
+  return CH_OK;
+}
+
 int ch_batch_schedule(ch_table* t, uint64_t n) {
   if (!t) return fail(CH_EINVAL, "null table");
   std::lock_guard<std::mutex> lock(t->mu);
@@ -580,6 +591,13 @@ int ch_multi_insert(ch_table* t, const void* keys, const void* vals, uint64_t n,
   if (t->cfg.kind != CH_MULTI) return fail(CH_EINVAL, "ch_multi_insert needs a multi-value table");
   if (n && (!keys || !vals || !status)) return fail(CH_EINVAL, "null buffer");
   Ordered o(t, stream);
+  if (n >= 4096 && t->group_mode != 1) {  // grouped: one sequence walk per distinct key (mgroup.cu)
+    Scratch sc(o.s);
+    const size_t bytes = mgroup_scratch_bytes(n, t->ts.kbytes, t->ts.vbytes);
+    void* p = sc.get(bytes);
+    if (!p) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+    return o.done(multi_insert_grouped(o.lc, t->T, t->ts, keys, vals, n, status, p, bytes));
+  }
   return o.done(multi_insert(o.lc, t->T, t->ts, keys, vals, n, status));
 }
 
@@ -589,7 +607,10 @@ int ch_multi_count(ch_table* t, const void* keys, uint64_t n, uint32_t* counts, 
   if (!offsets || (n && (!keys || !counts))) return fail(CH_EINVAL, "null buffer");
   Ordered o(t, stream);
   Scratch sc(o.s);
-  int rc = multi_scan(o.lc, t->T, t->ts, keys, n, counts, nullptr, nullptr, 0);
+  uint32_t* ll = (uint32_t*)sc.get(n * 4 + 16);
+  unsigned long long* lc2 = (unsigned long long*)sc.get(16);
+  if (!ll || !lc2) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+  int rc = multi_scan(o.lc, t->T, t->ts, keys, n, counts, nullptr, nullptr, 0, ll, lc2);
   if (!rc) {
     const size_t sb = exclusive_scan_scratch_bytes(n);
     void* p = sc.get(sb);
@@ -606,7 +627,11 @@ int ch_multi_retrieve(ch_table* t, const void* keys, uint64_t n, const uint64_t*
   if (n && (!keys || !offsets)) return fail(CH_EINVAL, "null buffer");
   Ordered o(t, stream);
   t->host_ops += n;
-  return o.done(multi_scan(o.lc, t->T, t->ts, keys, n, nullptr, offsets, vals_out, 1));
+  Scratch sc(o.s);
+  uint32_t* ll = (uint32_t*)sc.get(n * 4 + 16);
+  unsigned long long* lc2 = (unsigned long long*)sc.get(16);
+  if (!ll || !lc2) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+  return o.done(multi_scan(o.lc, t->T, t->ts, keys, n, nullptr, offsets, vals_out, 1, ll, lc2));
 }
 
 int ch_bucket_insert(ch_table* t, const void* keys, const void* vals, uint64_t n, uint8_t* status, void* stream) {

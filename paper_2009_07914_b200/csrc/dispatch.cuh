@@ -154,7 +154,8 @@ int single_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
 int multi_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, const void* vals,
                  uint64_t n, uint8_t* status);
 int multi_scan(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
-               uint32_t* counts, const uint64_t* offsets, void* vals_out, int mode);
+               uint32_t* counts, const uint64_t* offsets, void* vals_out, int mode, uint32_t* long_list,
+               unsigned long long* counters);
 int exclusive_scan_u32(const Launch& lc, const uint32_t* counts, uint64_t n, uint64_t* out, void* scratch,
                        size_t scratch_bytes);
 size_t exclusive_scan_scratch_bytes(uint64_t n);

@@ -89,11 +89,16 @@ __global__ void __launch_bounds__(256) k_multi_insert(TableRef T, const K* __res
 }
 
 // MODE 0: counts[i]; MODE 1: write values at offsets[i] (probe order)
+// Thread per query, 8-slot spans (bandwidth-lean for the many short chains).  Queries
+// still open after `budget` windows are handed to the warp walker (k_multi_walk) through
+// a device-counted list, unaccounted here (the walker restarts and accounts them).
 template <Layout LAY, typename K, typename V, int G, int MODE>
 __global__ void __launch_bounds__(256) k_multi_scan(TableRef T, const K* __restrict__ keys, uint64_t n,
                                                     uint32_t* __restrict__ counts,
                                                     const uint64_t* __restrict__ offsets,
-                                                    V* __restrict__ out) {
+                                                    V* __restrict__ out, uint32_t budget,
+                                                    uint32_t* __restrict__ long_list,
+                                                    unsigned long long* __restrict__ long_count) {
   using P = Probe<LAY, K, V, G>;
   using Ops = typename P::Ops;
   constexpr int MCHUNK = chunk_for<K, V>();
@@ -103,9 +108,13 @@ __global__ void __launch_bounds__(256) k_multi_scan(TableRef T, const K* __restr
   __shared__ uint8_t s_ho[MCHUNK];
   const StartSlots ss{s_hw, s_sw, s_ho};
   __shared__ uint32_t s_cnt[MODE == 0 ? MCHUNK : 1];
+  __shared__ uint32_t s_long[MCHUNK];
+  __shared__ uint32_t s_nlong;
+  __shared__ unsigned long long s_lbase;
   constexpr int lane = 0;  // one thread per key (probe.cuh)
   long long att = 0, win = 0;
   while (chunk_begin<MCHUNK>(cs, T.work, n)) {
+    if (threadIdx.x == 0) s_nlong = 0;
     stage_keys(s_keys, ss, keys, cs, T);
     __syncthreads();
     bool active = false;
@@ -156,6 +165,11 @@ __global__ void __launch_bounds__(256) k_multi_scan(TableRef T, const K* __restr
       } else if (!P::advance(T, cur, st, ps.step)) {
         done = true;
         attempts = cur.attempts;
+      } else if (budget && cur.j >= budget) {  // a long chain: to the warp walker
+        s_long[atomicAdd(&s_nlong, 1u)] = (uint32_t)(cs.base + li);
+        if (MODE == 0 && lane == 0) s_cnt[li] = 0;
+        active = false;
+        continue;
       }
       if (done) {
         if (MODE == 0 && lane == 0) s_cnt[li] = (uint32_t)total;
@@ -166,6 +180,128 @@ __global__ void __launch_bounds__(256) k_multi_scan(TableRef T, const K* __restr
     }
     __syncthreads();
     if (MODE == 0) stage_out(counts, s_cnt, cs);
+    if (long_list) {
+      if (threadIdx.x == 0) s_lbase = s_nlong ? atomicAdd(long_count, (unsigned long long)s_nlong) : 0ull;
+      __syncthreads();
+      for (uint32_t x = threadIdx.x; x < s_nlong; x += blockDim.x) long_list[s_lbase + x] = s_long[x];
+    }
+  }
+  // ops are accounted per bulk call on the host side (multi_table.py:249,290: ops += n)
+  const long long v[2] = {att, win};
+  long long* const dst[2] = {(long long*)&T.ctr->attempts, (long long*)&T.ctr->windows};
+  cta_add<2>(v, dst);
+}
+
+// K5 / K6 as one warp per query (the count pass and the write pass walk the same
+// sequence): a lane per slot of a 32-slot window, matches in window (= probe) order
+// before the first empty, tombstones passed (multi_table.py:171-203).  After the first
+// window the warp loads WW windows per step (independent loads) so a hot key's long
+// chain costs chain / (32 WW) dependent steps; windows after the first empty are read
+// but ignored.  A thread per query walked a 23K-copy chain alone (the batch's tail).
+template <Layout LAY, typename K, typename V>
+__device__ __forceinline__ uint64_t mw_load(const TableRef& T, uint64_t q) {
+  if constexpr (LAY == PACKED) return __ldcg(static_cast<const unsigned long long*>(T.slots) + q);
+  else if constexpr (LAY == SOA) return (uint64_t)__ldcg(static_cast<const K*>(T.slots) + q);
+  else return (uint64_t)__ldcg(&static_cast<const CellT<K, V>*>(T.slots)[q].k);
+}
+template <Layout LAY, typename K, typename V>
+__device__ __forceinline__ V mw_value(const TableRef& T, uint64_t q, uint64_t word) {
+  if constexpr (LAY == PACKED) return (V)(word >> 32);
+  else if constexpr (LAY == SOA) return __ldcg(static_cast<const V*>(T.vals) + q);
+  else return __ldcg(&static_cast<const CellT<K, V>*>(T.slots)[q].v);
+}
+
+template <Layout LAY, typename K, typename V, int MODE>
+__global__ void __launch_bounds__(256) k_multi_walk(TableRef T, const K* __restrict__ keys, uint64_t n,
+                                                    uint32_t* __restrict__ counts,
+                                                    const uint64_t* __restrict__ offsets, V* __restrict__ out,
+                                                    unsigned long long* __restrict__ next, int g,
+                                                    const uint32_t* __restrict__ list,
+                                                    const unsigned long long* __restrict__ n_dev) {
+  if (n_dev) n = *n_dev;
+  constexpr int WW = 4;
+  const int lane = threadIdx.x & 31;
+  const uint32_t below = (1u << lane) - 1u;
+  const K e = (K)T.e, tomb = (K)T.t;
+  const uint32_t ug = (uint32_t)g;
+  long long att = 0, win = 0;
+  for (;;) {
+    unsigned long long qi = 0;
+    if (lane == 0) qi = atomicAdd(next, 1ull);
+    qi = __shfl_sync(0xffffffffu, qi, 0);
+    if (qi >= n) break;
+    if (list) qi = list[qi];
+    const K k = keys[qi];
+    uint64_t base = 0, want = 0;
+    bool skip = k == e || k == tomb;
+    if (MODE == 1 && !skip) {  // nothing to collect (multi_table.py:279-280)
+      base = offsets[qi];
+      want = offsets[qi + 1] - base;
+      skip = want == 0;
+    }
+    if (skip) {
+      if (MODE == 0 && lane == 0) counts[qi] = 0;
+      continue;
+    }
+    const ProbeStart ps = probe_start(T, (uint64_t)k);
+    uint64_t ws = ps.h, total = 0, attempts = 0, windows = 0;
+    uint32_t j = 0, nw = 1;  // windows per step: 1 first, then WW
+    bool done = false;
+    while (!done) {
+      uint64_t w[WW];
+      uint64_t wsv[WW];
+      uint64_t s = ws;
+#pragma unroll
+      for (int v = 0; v < WW; ++v) {
+        wsv[v] = s;
+        if ((uint32_t)v < nw && j + v < T.max_windows) {
+          uint64_t q = s + lane;
+          if (q >= T.c) q -= T.c;
+          w[v] = mw_load<LAY, K, V>(T, q);
+        } else {
+          w[v] = 0;
+        }
+        s += ps.step;
+        if (s >= T.c) s -= T.c;
+      }
+#pragma unroll
+      for (int v = 0; v < WW; ++v) {
+        if (done || (uint32_t)v >= nw) continue;
+        if (j + v >= T.max_windows) {  // budget walked without an empty (probing.py:214-217)
+          attempts = (uint64_t)T.max_windows * WINDOW;
+          windows = T.max_windows;
+          done = true;
+          continue;
+        }
+        const K c = (K)w[v];
+        const uint32_t em = __ballot_sync(0xffffffffu, c == e);
+        const uint32_t km = __ballot_sync(0xffffffffu, c == k) & below_lowest(em);
+        if (MODE == 1 && ((km >> lane) & 1u)) {
+          const uint64_t r = total + __popc(km & below);
+          uint64_t q = wsv[v] + lane;
+          if (q >= T.c) q -= T.c;
+          if (r < want) out[base + r] = mw_value<LAY, K, V>(T, q, w[v]);  // racing writer: keep the length
+        }
+        total += __popc(km);
+        if (em) {
+          attempts = (uint64_t)(j + v) * WINDOW + chunk_end(lowest_bit(em), ug);
+          windows = j + v + 1;
+          done = true;
+        }
+      }
+      j += nw;
+      ws = wsv[0];
+      for (uint32_t v = 0; v < nw; ++v) {
+        ws += ps.step;
+        if (ws >= T.c) ws -= T.c;
+      }
+      nw = nw * 2 < (uint32_t)WW ? nw * 2 : (uint32_t)WW;  // 1, 2, 4, 4, ... windows per step
+    }
+    if (lane == 0) {
+      if (MODE == 0) counts[qi] = (uint32_t)total;
+      att += (long long)attempts;
+      win += (long long)windows;
+    }
   }
   // ops are accounted per bulk call on the host side (multi_table.py:249,290: ops += n)
   const long long v[2] = {att, win};
@@ -182,18 +318,35 @@ struct MultiKernels {
       kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status);
     });
   }
+  // thread pass (first kBudget windows), then the warp walker over the queries it handed off
+  static constexpr uint32_t kBudget = 4;
   static int scan(const Launch& lc, const TableRef& T, const void* keys, uint64_t n, uint32_t* counts,
-                  const uint64_t* offsets, void* out, int mode) {
+                  const uint64_t* offsets, void* out, int mode, uint32_t* long_list,
+                  unsigned long long* counters) {
+    if (n == 0) return 0;
+    int rc = cuda_check(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), lc.stream), "memset");
+    if (rc) return rc;
     if (mode == 0) {
       auto kern = k_multi_scan<LAY, K, V, G, 0>;
-      return launch_chunked(lc, T, (const void*)kern, n, (chunk_for<K, V>()), [&](dim3 g, dim3 b) {
-        kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out);
+      rc = launch_chunked(lc, T, (const void*)kern, n, (chunk_for<K, V>()), [&](dim3 g, dim3 b) {
+        kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out, kBudget, long_list, counters);
+      });
+    } else {
+      auto kern = k_multi_scan<LAY, K, V, G, 1>;
+      rc = launch_chunked(lc, T, (const void*)kern, n, (chunk_for<K, V>()), [&](dim3 g, dim3 b) {
+        kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out, kBudget, long_list, counters);
       });
     }
-    auto kern = k_multi_scan<LAY, K, V, G, 1>;
-    return launch_chunked(lc, T, (const void*)kern, n, (chunk_for<K, V>()), [&](dim3 g, dim3 b) {
-      kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out);
-    });
+    if (rc) return rc;
+    const unsigned grid = (unsigned)(lc.sms * 8);
+    if (mode == 0)
+      k_multi_walk<LAY, K, V, 0><<<grid, 256, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out,
+                                                             counters + 1, G, long_list, counters);
+    else
+      k_multi_walk<LAY, K, V, 1><<<grid, 256, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out,
+                                                             counters + 1, G, long_list, counters);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "multi walk");
   }
 };
 
@@ -203,9 +356,10 @@ int multi_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const v
       ts, [&](auto tag) { return decltype(tag)::type::insert(lc, T, keys, vals, n, status); });
 }
 int multi_scan(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
-               uint32_t* counts, const uint64_t* offsets, void* vals_out, int mode) {
+               uint32_t* counts, const uint64_t* offsets, void* vals_out, int mode, uint32_t* long_list,
+               unsigned long long* counters) {
   return dispatch_types<MultiKernels>(ts, [&](auto tag) {
-    return decltype(tag)::type::scan(lc, T, keys, n, counts, offsets, vals_out, mode);
+    return decltype(tag)::type::scan(lc, T, keys, n, counts, offsets, vals_out, mode, long_list, counters);
   });
 }
 

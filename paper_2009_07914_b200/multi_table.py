@@ -66,6 +66,11 @@ class MultiValueHashTable(_TableBase):
         self._dt.touch()
         return st
 
+    def set_grouping(self, on: bool) -> None:
+        """Bulk inserts of >= 4096 pairs group the batch by key first and walk each distinct
+        key's sequence once (csrc/mgroup.cu); off = the reference's pair-by-pair order."""
+        _lib.check(_lib.lib().ch_set_multi_grouping(self._dt.handle, int(bool(on))), "set_grouping")
+
     def count_device(self, keys, stream=None) -> tuple[torch.Tensor, torch.Tensor]:
         """Counting pass + device exclusive scan: (counts int32, offsets int64[n+1])."""
         k = self._keys(keys)
