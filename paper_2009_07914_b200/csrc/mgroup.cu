@@ -17,6 +17,7 @@
 // counters are computed from the sequence positions, exactly as the reference counts
 // them (single_table.py:197).
 #include <cub/device/device_radix_sort.cuh>
+#include <cstdlib>
 #include <type_traits>
 
 #include "dispatch.cuh"
@@ -89,29 +90,51 @@ __device__ __forceinline__ void mg_store_value(const TableRef& T, uint64_t q, V 
   }
 }
 
-// One warp per distinct key (groups taken from a global counter): walk the key's
-// sequence window by window and claim the group's m cells in sequence order.  Statuses
-// are pre-set to INSERTED; copies that find the sequence exhausted become TABLE_FULL,
+// Big groups first: their index list (m >= MG_BIG), so the longest walks start while the
+// table is emptiest and no hot key is left as the kernel's tail.
+constexpr uint32_t MG_BIG = 256;
+__global__ void k_mg_big(const uint32_t* __restrict__ gstart, const uint64_t* __restrict__ ngroups_p,
+                         uint32_t* __restrict__ big, unsigned long long* __restrict__ nbig) {
+  const uint64_t ng = *ngroups_p;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += stride)
+    if (gstart[i + 1] - gstart[i] >= MG_BIG) big[atomicAdd(nbig, 1ull)] = (uint32_t)i;
+}
+
+// One warp per distinct key (big groups first, then the rest in sorted order, taken from
+// a global counter): walk the key's sequence and claim the group's m cells in sequence
+// order -- one window per step while few copies remain, MW windows per step (independent
+// loads, claims assigned across the windows in order) while many do.  Statuses are
+// pre-set to INSERTED; copies that find the sequence exhausted become TABLE_FULL,
 // sentinel keys INVALID_KEY.
 template <Layout LAY, typename K, typename V, typename P>
 __global__ void __launch_bounds__(MG_THREADS) k_mg_place(TableRef T, const K* __restrict__ sk,
                                                          const P* __restrict__ sidx,
                                                          const uint32_t* __restrict__ gstart,
                                                          const uint64_t* __restrict__ ngroups_p,
+                                                         const uint32_t* __restrict__ big,
+                                                         const unsigned long long* __restrict__ nbig_p,
                                                          unsigned long long* __restrict__ next,
                                                          const V* __restrict__ vals, uint8_t* __restrict__ status,
-                                                         int g) {
+                                                         int g, int mw_max) {
+  constexpr int MW = 4;
   const int lane = threadIdx.x & 31;
   const uint32_t below = (1u << lane) - 1u;
   const K e = (K)T.e, tomb = (K)T.t;
   const uint32_t ug = (uint32_t)g;
-  const uint64_t ngroups = *ngroups_p;
+  const uint64_t ngroups = *ngroups_p, nbig = *nbig_p;
   long long ops = 0, att = 0, win = 0, occ = 0;
   for (;;) {
     unsigned long long gi = 0;
     if (lane == 0) gi = atomicAdd(next, 1ull);
     gi = __shfl_sync(0xffffffffu, gi, 0);
-    if (gi >= ngroups) break;
+    if (gi >= nbig + ngroups) break;
+    if (gi < nbig) {
+      gi = big[gi];
+    } else {
+      gi -= nbig;
+      if (gstart[gi + 1] - gstart[gi] >= MG_BIG) continue;  // done in the big-group phase
+    }
     const uint32_t base = gstart[gi], m = gstart[gi + 1] - base;
     const K k = sk[base];
     if (k == e || k == tomb) {  // INVALID_KEY, no accounting (multi_table.py:213-215)
@@ -121,34 +144,73 @@ __global__ void __launch_bounds__(MG_THREADS) k_mg_place(TableRef T, const K* __
     const ProbeStart ps = probe_start(T, (uint64_t)k);
     uint64_t ws = ps.h;
     uint32_t j = 0, o = 0, placed = 0;
-    while (placed < m) {
-      uint64_t q = ws + lane;
-      if (q >= T.c) q -= T.c;
-      const K c = mg_key<LAY, K, V>(T, q);
-      const bool fr = (uint32_t)lane >= o && (c == e || c == tomb);  // lowest free first (:136-139)
-      const uint32_t fm = __ballot_sync(0xffffffffu, fr);
-      const uint32_t want = m - placed;
-      const bool sel = fr && __popc(fm & below) < want;
-      const bool won = sel && mg_claim<LAY, K, V>(T, q, c, k);
-      const uint32_t wm = __ballot_sync(0xffffffffu, won);
-      if (won) {
-        const uint32_t idx = placed + __popc(wm & below);
-        const P pv = sidx[base + idx];
-        mg_store_value<LAY, K, V>(T, q, sizeof(P) == 8 ? (V)(uint32_t)pv : vals[pay_idx(pv)]);
-        att += (long long)((uint64_t)j * WINDOW + chunk_end((uint32_t)lane, ug));
-        win += (long long)(j + 1);
+    bool exhausted = false;
+    while (placed < m && !exhausted) {
+      const uint32_t nw = m - placed > 32 ? (uint32_t)mw_max : 1u;
+      K c[MW];
+      uint64_t wsv[MW];
+      uint64_t sv = ws;
+#pragma unroll
+      for (int v = 0; v < MW; ++v) {  // independent loads of nw windows
+        wsv[v] = sv;
+        c[v] = k;  // "not free"
+        if ((uint32_t)v < nw && j + v < T.max_windows) {
+          uint64_t q = sv + lane;
+          if (q >= T.c) q -= T.c;
+          c[v] = mg_key<LAY, K, V>(T, q);
+        }
+        sv += ps.step;
+        if (sv >= T.c) sv -= T.c;
       }
-      placed += __popc(wm);
-      const uint32_t sm = __ballot_sync(0xffffffffu, sel);
-      // continue after the last cell this step tried (lost ones are occupied now)
-      o = sm ? 32u - __clz(sm) : 32u;
-      if (o >= WINDOW && placed < m) {
+      uint32_t taken = 0, last_v = 0, last_sel = 0;
+      bool any_sel = false, stop = false;
+#pragma unroll
+      for (int v = 0; v < MW; ++v) {
+        // a lost claim ends the step: its copy belongs to the next free cell in sequence
+        // order, which may be a later cell of the same window (not one of a later window)
+        if ((uint32_t)v >= nw || stop) continue;
+        const bool fr = (v > 0 || (uint32_t)lane >= o) && (c[v] == e || c[v] == tomb);  // lowest free first
+        const uint32_t fm = __ballot_sync(0xffffffffu, fr);
+        const uint32_t want = m - placed - taken;
+        const bool sel = fr && __popc(fm & below) < want;
+        uint64_t q = wsv[v] + lane;
+        if (q >= T.c) q -= T.c;
+        const bool won = sel && mg_claim<LAY, K, V>(T, q, c[v], k);
+        const uint32_t wm = __ballot_sync(0xffffffffu, won);
+        if (won) {
+          const uint32_t idx = placed + taken + __popc(wm & below);
+          const P pv = sidx[base + idx];
+          mg_store_value<LAY, K, V>(T, q, sizeof(P) == 8 ? (V)(uint32_t)pv : vals[pay_idx(pv)]);
+          att += (long long)((uint64_t)(j + v) * WINDOW + chunk_end((uint32_t)lane, ug));
+          win += (long long)(j + v + 1);
+        }
+        taken += __popc(wm);
+        const uint32_t sm = __ballot_sync(0xffffffffu, sel);
+        if (sm) {
+          any_sel = true;
+          last_v = (uint32_t)v;
+          last_sel = 32u - __clz(sm);
+        }
+        if (sm != wm) stop = true;
+      }
+      placed += taken;
+      if (placed >= m) break;
+      // continue after the last cell tried (lost ones are occupied now); windows whose
+      // free cells were all taken are behind us
+      uint32_t adv;
+      if (any_sel && last_sel < WINDOW) {
+        adv = last_v;
+        o = last_sel;
+      } else {
+        adv = any_sel ? last_v + 1 : nw;
         o = 0;
+      }
+      for (uint32_t v = 0; v < adv; ++v) {
         ++j;
-        if (j >= T.max_windows) break;
         ws += ps.step;
         if (ws >= T.c) ws -= T.c;
       }
+      if (j >= T.max_windows) exhausted = true;
     }
     if (lane == 0) {
       ops += m;
@@ -166,6 +228,11 @@ __global__ void __launch_bounds__(MG_THREADS) k_mg_place(TableRef T, const K* __
 }
 
 static uint64_t al256(uint64_t x) { return (x + 255) & ~(uint64_t)255; }
+static int g_mw = [] {
+  const char* e = getenv("CH_MG_MW");
+  const int v = e ? atoi(e) : 4;
+  return v >= 1 && v <= 4 ? v : 4;
+}();
 
 template <typename K, typename P>
 static size_t sort_temp_bytes(uint64_t n) {
@@ -179,7 +246,7 @@ size_t mgroup_scratch_bytes(uint64_t n, int kbytes, int vbytes) {
   const size_t sort_b = kbytes == 8 ? sort_temp_bytes<uint64_t, uint64_t>(n) : sort_temp_bytes<uint32_t, uint64_t>(n);
   (void)vbytes;
   return al256(sort_b) + al256(n * kbytes) + 2 * al256(n * 8) + al256(n * 4) + al256((n + 1) * 8) +
-         al256(exclusive_scan_scratch_bytes(n)) + al256((n + 1) * 4) + 256;
+         al256(exclusive_scan_scratch_bytes(n)) + 2 * al256((n + 1) * 4) + 256;
 }
 
 template <Layout LAY, typename K, typename V>
@@ -206,13 +273,14 @@ static int mgroup_impl(const Launch& lc, const TableRef& T, int g, const K* keys
   const size_t scan_b = exclusive_scan_scratch_bytes(n);
   void* scan = take(scan_b);
   uint32_t* gstart = (uint32_t*)take((n + 1) * 4);
-  unsigned long long* next = (unsigned long long*)take(64);
+  uint32_t* big = (uint32_t*)take((n + 1) * 4);
+  unsigned long long* next = (unsigned long long*)take(64);  // [0] work counter, [1] big groups
   if ((size_t)(q - static_cast<char*>(scratch)) > scratch_bytes) {
     set_error("grouped insert scratch too small");
     return -22;
   }
   int rc = cuda_check(cudaMemsetAsync(status, ST_INSERTED, n, lc.stream), "memset");
-  if (!rc) rc = cuda_check(cudaMemsetAsync(next, 0, 8, lc.stream), "memset");
+  if (!rc) rc = cuda_check(cudaMemsetAsync(next, 0, 16, lc.stream), "memset");
   if (rc) return rc;
   const unsigned grid = (unsigned)(lc.sms * 8);
   k_mg_payload<P, V><<<grid, MG_THREADS, 0, lc.stream>>>(idx, vals, n);
@@ -227,12 +295,14 @@ static int mgroup_impl(const Launch& lc, const TableRef& T, int g, const K* keys
   if ((rc = exclusive_scan_u32(lc, head, n, hoff, scan, scan_b))) return rc;
   k_mg_starts<<<grid, MG_THREADS, 0, lc.stream>>>(head, hoff, n, gstart);
   count_launch();
+  k_mg_big<<<grid, MG_THREADS, 0, lc.stream>>>(gstart, hoff + n, big, next + 1);
+  count_launch();
   if ((rc = cuda_check(cudaGetLastError(), "group runs"))) return rc;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (lc.timer && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess)
     cudaEventRecord(e0, lc.stream);
-  k_mg_place<LAY, K, V, P><<<grid, MG_THREADS, 0, lc.stream>>>(T, sk, sidx, gstart, hoff + n, next, vals, status,
-                                                                g);
+  k_mg_place<LAY, K, V, P><<<grid, MG_THREADS, 0, lc.stream>>>(T, sk, sidx, gstart, hoff + n, big, next + 1, next,
+                                                                vals, status, g, g_mw);
   count_launch();
   if (e1) {
     cudaEventRecord(e1, lc.stream);
