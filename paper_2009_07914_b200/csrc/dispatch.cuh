@@ -34,6 +34,8 @@ struct Launch {
   // cap on the CTAs of a chunk-scheduled kernel (0: one full wave).  A narrower
   // wave keeps the in-flight band of a region-ordered batch inside L2.
   int max_blocks = 0;
+  // optional device counter of non-INSERTED statuses written by an insert
+  unsigned long long* exc = nullptr;
 };
 
 struct TypeSel {

@@ -50,11 +50,13 @@ __global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restri
                                                 int64_t* __restrict__ slot_out,
                                                 const unsigned long long* __restrict__ n_dev,
                                                 const uint32_t* __restrict__ out_idx,
-                                                const uint32_t* __restrict__ o_start) {
+                                                const uint32_t* __restrict__ o_start,
+                                                unsigned long long* __restrict__ exc) {
   if (n_dev) n = *n_dev;
   using P = Probe<LAY, K, V, G>;
   using Ops = typename P::Ops;
   constexpr int CHUNK = insert_chunk<K, V, MODE>();
+  long long nexc = 0;  // statuses other than INSERTED (staged.cu skips its status gathers without any)
   __shared__ ChunkState cs;
   __shared__ K s_keys[CHUNK];
   __shared__ uint32_t s_hw[CHUNK], s_sw[CHUNK];
@@ -249,11 +251,13 @@ __global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restri
     __syncthreads();
     stage_out_ix(status, s_status, cs, out_idx);
     if (MODE == 1) stage_out(slot_out, s_slot, cs);
+    if (exc)
+      for (uint32_t j = threadIdx.x; j < cs.cnt; j += blockDim.x) nexc += s_status[j] != ST_INSERTED;
   }
-  const long long v[5] = {ops, att, win, occ, tomb};
-  long long* const dst[5] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts,
-                             (long long*)&T.ctr->windows, &T.ctr->occupied, &T.ctr->tombstones};
-  cta_add<5>(v, dst);
+  const long long v[6] = {ops, att, win, occ, tomb, nexc};
+  long long* const dst[6] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts,
+                             (long long*)&T.ctr->windows, &T.ctr->occupied, &T.ctr->tombstones, (long long*)exc};
+  cta_add<6>(v, dst);
 }
 
 // ------------------------------------------------------------------ K2
@@ -439,13 +443,13 @@ struct SingleKernels {
       auto kern = k_insert<LAY, K, V, G, 0>;
       return launch_chunked(lc, T, (const void*)kern, n, insert_chunk<K, V, 0>(), [&](dim3 g, dim3 b) {
         kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status, slot_out, lc.n_dev,
-                                     lc.out_idx, lc.o_start);
+                                     lc.out_idx, lc.o_start, lc.exc);
       });
     }
     auto kern = k_insert<LAY, K, V, G, 1>;
     return launch_chunked(lc, T, (const void*)kern, n, insert_chunk<K, V, 1>(), [&](dim3 g, dim3 b) {
       kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status, slot_out, lc.n_dev,
-                                     lc.out_idx, lc.o_start);
+                                     lc.out_idx, lc.o_start, lc.exc);
     });
   }
   static int lookup(const Launch& lc, const TableRef& T, const void* keys, uint64_t n, void* vals_out,

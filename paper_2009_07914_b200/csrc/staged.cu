@@ -357,7 +357,8 @@ __global__ void __launch_bounds__(PT) k_st_gather(uint64_t n, const uint64_t* __
                                                   const uint16_t* __restrict__ th, const uint32_t* __restrict__ tg,
                                                   uint32_t nb, const uint32_t* __restrict__ src_v,
                                                   const uint8_t* __restrict__ src_f, uint32_t* __restrict__ dst_v,
-                                                  uint8_t* __restrict__ dst_f) {
+                                                  uint8_t* __restrict__ dst_f,
+                                                  const unsigned long long* __restrict__ exc) {
   __shared__ uint32_t sV[VAL ? PTILE : 1];
   __shared__ uint8_t sF[PTILE];
   __shared__ uint16_t sB[PTILE];
@@ -371,6 +372,11 @@ __global__ void __launch_bounds__(PT) k_st_gather(uint64_t n, const uint64_t* __
   }
   TileGeo g;
   if (t >= ntiles || !tile_geo<L>(t, n, foff, s_ts, supers, regions, g)) return;
+  if (!VAL && exc && *exc == 0) {  // every status is INSERTED: nothing to move back
+    if (L == 1)
+      for (uint32_t li = threadIdx.x; li < g.cnt; li += PT) dst_f[g.pos0 + li] = ST_INSERTED;
+    return;
+  }
   const uint32_t hv = threadIdx.x < nb ? th[(uint64_t)t * nb + threadIdx.x] : 0u;
   const uint32_t gs = threadIdx.x < nb ? tg[(uint64_t)t * nb + threadIdx.x] : 0u;
   uint16_t iv[PI];
@@ -523,7 +529,8 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
                                                     const uint32_t* __restrict__ pos,
                                                     const uint16_t* __restrict__ los, uint8_t* __restrict__ status,
                                                     uint32_t* __restrict__ res_val, uint8_t* __restrict__ res_flag,
-                                                    DeferOut DA, DeferOut DB, int g) {
+                                                    DeferOut DA, DeferOut DB, int g,
+                                                    unsigned long long* __restrict__ exc) {
   constexpr bool INS = MODE == 0;
   constexpr uint32_t HALO = INS ? 0u : ST_HALO;
   constexpr uint32_t OW = R2 ? WINDOW : 0u;  // sequence offset of the window probed here
@@ -560,7 +567,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
   __syncthreads();  // the mbarrier is initialised before anyone waits on it
   const uint32_t e = (uint32_t)T.e, t = (uint32_t)T.t;
   const uint32_t ug = (uint32_t)g;
-  long long ops = 0, att = 0, win = 0, occ = 0, ndef = 0;
+  long long ops = 0, att = 0, win = 0, occ = 0, ndef = 0, nexc = 0;
   bool claimed_any = false, waited = false;
 
   // Sentinel test: with the default sentinels (t = e - 1) "free" is one subtract
@@ -599,6 +606,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
     if (INS) {
       if (c == k) {  // present before the first free cell (single_table.py:198-200)
         status[ri] = ST_DUPLICATE;
+        nexc += 1;
       } else if (c == t) {  // tombstone first: the deferred-claim rule (:201-223), COPS kernel
         defer_push(BA, DA, k, s_val[i], ri, OW);
         ndef += 1;
@@ -669,6 +677,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
         if (k == e || k == t) {  // sentinels are never stored (single_table.py:369-370, 391-393)
           if (INS) {
             status[s0 + i] = ST_INVALID;
+            nexc += 1;
           } else {
             res_val[s0 + i] = 0;
             res_flag[s0 + i] = 0;
@@ -707,9 +716,9 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
     __syncthreads();
     if (threadIdx.x == 0 && dirty) bulk_store_wait(slots + rbase, tile, len * 8u);
   }
-  const long long v[6] = {ops, att, win, occ, 0, ndef};
+  const long long v[6] = {ops, att, win, occ, nexc, ndef};
   long long* const dst[6] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
-                             &T.ctr->occupied, nullptr, (long long*)&T.ctr->deferred};
+                             &T.ctr->occupied, INS ? (long long*)exc : nullptr, (long long*)&T.ctr->deferred};
   cta_add<6>(v, dst);
 }
 
@@ -908,23 +917,24 @@ static int st_forward(const Launch& lc, const TableRef& T, const StPlan& p, cons
 // region-ordered results -> caller's order (inverse of L2, then of L1)
 template <bool VAL>
 static int st_backward(const Launch& lc, const StPlan& p, const StBufs& b, uint64_t n, const uint32_t* rv,
-                       const uint8_t* rf, uint32_t* out_v, uint8_t* out_f) {
+                       const uint8_t* rf, uint32_t* out_v, uint8_t* out_f, const unsigned long long* exc = nullptr) {
   const Round& r = b.r1;
   const unsigned t1 = (unsigned)p.tiles1, t2 = (unsigned)p.tiles2;
   auto g2 = k_st_gather<2, VAL>;
   auto g1 = k_st_gather<1, VAL>;
   g2<<<t2, PT, 0, lc.stream>>>(n, r.foff, r.tstart, p.supers, p.regions, t2, r.inv2, r.th2, r.tg2, 256, rv, rf, b.rv1,
-                                b.rf1);
+                                b.rf1, exc);
   count_launch();
   g1<<<t1, PT, 0, lc.stream>>>(n, r.foff, r.tstart, p.supers, p.regions, t1, r.inv1, r.th1, r.tg1, p.supers, b.rv1,
-                                b.rf1, out_v, out_f);
+                                b.rf1, out_v, out_f, exc);
   count_launch();
   return cuda_check(cudaGetLastError(), "staged gather");
 }
 
 template <int MODE, bool R2>
 static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const Round& r, const uint32_t* pos,
-                    uint8_t* status, uint32_t* rv, uint8_t* rf, const DeferOut& DA, const DeferOut& DB, int g) {
+                    uint8_t* status, uint32_t* rv, uint8_t* rf, const DeferOut& DA, const DeferOut& DB, int g,
+                    unsigned long long* exc = nullptr) {
   const size_t sm = probe_smem<MODE, R2>();
   auto kern = k_st_probe<MODE, R2>;
   int rc = st_smem(kern, sm);
@@ -932,7 +942,7 @@ static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const 
   cudaEvent_t e0;
   if (!R2) st_timed(lc, &e0);  // the dominant kernel of the staged schedule (bench.py roofline)
   kern<<<p.regions, RT, sm, lc.stream>>>(T, r.foff, r.k2, MODE == 0 ? r.v2 : nullptr, pos, r.lo2, status, rv, rf, DA,
-                                         DB, g);
+                                         DB, g, exc);
   count_launch();
   if (!R2) st_timed_end(lc, e0);
   return cuda_check(cudaGetLastError(), "staged region probe");
@@ -944,17 +954,18 @@ int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
   size_t total = 0;
   const bool r2 = g_round2;
   const StBufs b = st_carve(p, n, true, r2, scratch, &total);
-  int rc = cuda_check(cudaMemsetAsync(b.dcount, 0, 16, lc.stream), "memset");
+  int rc = cuda_check(cudaMemsetAsync(b.dcount, 0, 24, lc.stream), "memset");  // lists A, B; exceptions
+  unsigned long long* exc = b.dcount + 2;
   if (!rc)
     rc = st_forward<1>(lc, T, p, b.r1, (const uint32_t*)keys, (const uint32_t*)vals, nullptr, nullptr, n, nullptr, 0,
                        2);
   if (rc) return rc;
   const DeferOut DA{b.ak, b.av, b.ax, b.ao, b.dcount};
   const DeferOut DB{b.bk, b.bv, b.bx, b.bo, r2 ? b.dcount + 1 : b.dcount};
-  if ((rc = st_probe<0, false>(lc, T, p, b.r1, nullptr, b.rf, nullptr, nullptr, DA, DB, ts.g))) return rc;
+  if ((rc = st_probe<0, false>(lc, T, p, b.r1, nullptr, b.rf, nullptr, nullptr, DA, DB, ts.g, exc))) return rc;
   if (r2) {  // window 1 of the keys whose window 0 was full, staged the same way
     if ((rc = st_forward<2>(lc, T, p, b.r2, b.bk, b.bv, b.bx, nullptr, n, b.dcount + 1, 1, 2))) return rc;
-    if ((rc = st_probe<0, true>(lc, T, p, b.r2, b.r2.p2, b.rf, nullptr, nullptr, DA, DA, ts.g))) return rc;
+    if ((rc = st_probe<0, true>(lc, T, p, b.r2, b.r2.p2, b.rf, nullptr, nullptr, DA, DA, ts.g, exc))) return rc;
   }
   // the rest: COPS kernels over the deferred keys ordered by their window-1 super-region
   // (consecutive CTAs probe one L2-resident stretch of the table), statuses to their
@@ -966,8 +977,9 @@ int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
   rest.out_idx = b.rd.p1;
   rest.o_start = b.rd.r1;
   rest.max_blocks = g_fb_blocks * lc.sms;
+  rest.exc = exc;
   if ((rc = single_insert(rest, T, ts, b.rd.k1, b.rd.v1, n, b.rf, nullptr, 0))) return rc;
-  return st_backward<false>(lc, p, b, n, nullptr, b.rf, nullptr, status);
+  return st_backward<false>(lc, p, b, n, nullptr, b.rf, nullptr, status, exc);
 }
 
 int staged_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
