@@ -767,7 +767,7 @@ struct Round {
   uint64_t* foff;
   void* scan;
   size_t scan_bytes;
-  uint32_t *k1, *v1, *p1, *r1, *k2, *v2, *p2;  // level-1 / level-2 outputs (payloads v, p, r)
+  uint32_t *k1, *v1, *p1, *r1, *k2, *v2, *p2, *r2;  // level-1 / level-2 outputs (payloads v, p, r)
   uint16_t* lo2;
   uint16_t *inv1, *inv2, *th1, *th2;  // inverse (round 1 only)
   uint32_t *tg1, *tg2;
@@ -798,6 +798,7 @@ static void carve_round(Carver& c, Round& r, const StPlan& p, uint64_t n, int np
     r.k2 = (uint32_t*)c.take(n * 4);
     r.v2 = npay >= 1 ? (uint32_t*)c.take(n * 4) : nullptr;
     r.p2 = npay >= 2 ? (uint32_t*)c.take(n * 4) : nullptr;
+    r.r2 = npay >= 3 ? (uint32_t*)c.take(n * 4) : nullptr;
     r.lo2 = (uint16_t*)c.take(n * 2);
   }
   if (inverse) {
@@ -905,10 +906,10 @@ static int st_forward(const Launch& lc, const TableRef& T, const StPlan& p, cons
                                    nullptr, r.inv1, r.th1, r.tg1, p.supers, r.cur1, n_dev, wj);
   count_launch();
   if (levels == 2) {
-    auto k2f = k_st_split<2, NPAY < 2 ? NPAY : 2>;
+    auto k2f = k_st_split<2, NPAY>;
     if ((rc = st_smem(k2f, sm2))) return rc;
-    k2f<<<t2, PT, sm2, lc.stream>>>(T, n, r.foff, r.tstart, p.supers, p.regions, t2, r.k1, r.v1, r.p1, nullptr, r.k2,
-                                     r.v2, r.p2, nullptr, r.lo2, r.inv2, r.th2, r.tg2, 256, r.cur2, n_dev, wj);
+    k2f<<<t2, PT, sm2, lc.stream>>>(T, n, r.foff, r.tstart, p.supers, p.regions, t2, r.k1, r.v1, r.p1, r.r1, r.k2,
+                                     r.v2, r.p2, r.r2, r.lo2, r.inv2, r.th2, r.tg2, 256, r.cur2, n_dev, wj);
     count_launch();
   }
   return cuda_check(cudaGetLastError(), "staged partition");
@@ -998,7 +999,8 @@ int staged_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
     if ((rc = st_forward<1>(lc, T, p, b.r2, b.bk, b.bx, nullptr, nullptr, n, b.dcount + 1, 1, 2))) return rc;
     if ((rc = st_probe<1, true>(lc, T, p, b.r2, b.r2.v2, nullptr, b.rv, b.rf, DA, DA, ts.g))) return rc;
   }
-  // deferred keys ordered by window-1 super-region (payloads: position, resume offset)
+  // deferred keys ordered by window-1 super-region (payloads: position, resume offset; a
+  // second, region-level split measured no better: the deferred keys are too sparse to share lines)
   if ((rc = st_forward<2>(lc, T, p, b.rd, b.ak, b.ax, b.ao, nullptr, n, b.dcount, 1, 1))) return rc;
   Launch rest = lc;
   rest.timer = nullptr;
