@@ -489,3 +489,37 @@ def test_host_pipeline_matches_device_path():
     assert f[:n].all() and (v[:n] == vals.astype(np.uint32)).all()
     dv, df = t.retrieve_device(keys[:4096])
     assert (dv.cpu().numpy().view(np.uint32) == v[:4096]).all()
+
+
+def test_staged_round2_and_fallback_caps_match_direct(tmp_path):
+    """The optional staged window-1 round (CH_STAGED_ROUND2=1) and a capped COPS pass
+    (CH_STAGED_FB_CTAS=1) give the same statuses / values / found flags as direct probes
+    (run in a child process: the switches are read when the library loads)."""
+    import subprocess
+    import sys
+    script = tmp_path / "r2.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {str(__import__('os').getcwd())!r})\n"
+        "from paper_2009_07914_b200 import SingleValueHashTable\n"
+        "n = 1 << 20\n"
+        "rng = np.random.default_rng(77)\n"
+        "pool = rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=3 * n, dtype=np.uint64)))\n"
+        "keys, absent = pool[:n], pool[n:2 * n]\n"
+        "vals = rng.integers(0, 1 << 32, size=n, dtype=np.uint64)\n"
+        "out = []\n"
+        "for loc in ('staged', 'off'):\n"
+        "    t = SingleValueHashTable(int(n / 0.97), layout='packed', key_bits=32, value_bits=32, group_width=8)\n"
+        "    t.set_locality(loc)\n"
+        "    st = t.insert_device(keys, vals).cpu().numpy()\n"
+        "    q = np.concatenate([keys, absent])\n"
+        "    v, f = t.retrieve_device(q)\n"
+        "    out.append((st, v.cpu().numpy(), f.cpu().numpy(), t.occupied))\n"
+        "a, b = out\n"
+        "assert (a[0] == 0).all() and (b[0] == 0).all() and a[3] == b[3] == n\n"
+        "assert (a[1] == b[1]).all() and (a[2] == b[2]).all() and a[2][:n].all() and not a[2][n:].any()\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, CH_STAGED_ROUND2="1", CH_STAGED_FB_CTAS="1")
+    r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
