@@ -80,6 +80,7 @@ struct ch_table {
   unsigned long long* bump = nullptr;  // also holds first_fail at [1]
   uint32_t* bcnt = nullptr;
   BucketInfo* info = nullptr;
+  ulonglong2* winfo = nullptr;
   uint64_t* gsizes = nullptr;
   uint64_t* gsums = nullptr;
   uint64_t gm = 0;
@@ -176,6 +177,7 @@ BucketRef bucket_ref(ch_table* t) {
   B.bump = t->bump;
   B.bcnt = t->bcnt;
   B.info = t->info;
+  B.winfo = t->winfo;
   B.first_fail = t->bump + 1;
   B.gr.sizes = t->gsizes;
   B.gr.sums = t->gsums;
@@ -366,6 +368,7 @@ int ch_create(ch_table** out, const ch_config* cfg) {
     if (cudaMalloc(&t->bump, 2 * sizeof(unsigned long long)) != cudaSuccess) return cleanup(CH_ENOMEM, "bump alloc");
     if (cudaMalloc(&t->bcnt, cap * sizeof(uint32_t)) != cudaSuccess) return cleanup(CH_ENOMEM, "batch count alloc");
     if (cudaMalloc(&t->info, cap * sizeof(BucketInfo)) != cudaSuccess) return cleanup(CH_ENOMEM, "bucket info alloc");
+    if (cudaMalloc(&t->winfo, cap * sizeof(ulonglong2)) != cudaSuccess) return cleanup(CH_ENOMEM, "bucket info alloc");
     if (cudaMalloc(&t->gsizes, t->gm * 8) != cudaSuccess || cudaMalloc(&t->gsums, t->gm * 8) != cudaSuccess)
       return cleanup(CH_ENOMEM, "growth table alloc");
     if (cudaMemcpy(t->gsizes, sizes.data(), t->gm * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -394,6 +397,7 @@ int ch_destroy(ch_table* t) {
   cudaFree(t->bump);
   cudaFree(t->bcnt);
   cudaFree(t->info);
+  cudaFree(t->winfo);
   cudaFree(t->gsizes);
   cudaFree(t->gsums);
   if (t->last) cudaEventDestroy(t->last);

@@ -105,7 +105,10 @@ __global__ void k_bucket_alloc(BucketRef B, Layout lay, const uint64_t* __restri
     BucketInfo in = B.info[s];
     uint64_t* hp = handle_ptr<K>(B.T, lay, s);
     const uint64_t h = *hp;
-    if ((h >> (COUNT_BITS + TAIL_BITS)) == H_FULL) continue;
+    if ((h >> (COUNT_BITS + TAIL_BITS)) == H_FULL) {  // sticky FULL: nothing fits
+      B.winfo[s] = make_ulonglong2(in.region | ((uint64_t)in.c0 << TAIL_BITS), in.tail_old);
+      continue;
+    }
     uint64_t tail = in.tail_old;
     if (in.need) {
       const uint64_t off = bump0 + alloc_off[s];
@@ -118,7 +121,10 @@ __global__ void k_bucket_alloc(BucketRef B, Layout lay, const uint64_t* __restri
       const uint64_t b1 = B.gr.buckets_for(in.new_count) - 1;
       tail = link_buckets(B, off, b0, b1, in.tail_old, vbytes);
       B.info[s].region = off;
+      in.region = off;
     }
+    B.winfo[s] = make_ulonglong2(in.region | ((uint64_t)in.c0 << TAIL_BITS),
+                                 in.tail_old | ((uint64_t)in.fit << TAIL_BITS));
     *hp = pack_handle(in.overflow ? H_FULL : H_READY, in.new_count, tail);
     values += in.fit;
   }
@@ -164,6 +170,8 @@ __global__ void k_bucket_alloc_seq(BucketRef B, Layout lay, const uint64_t* __re
     const uint64_t count = in.c0 + (fit < in.fit ? fit : in.fit);
     B.info[s].fit = (uint32_t)(fit < in.fit ? fit : in.fit);
     B.info[s].region = region;
+    B.winfo[s] = make_ulonglong2(region | ((uint64_t)in.c0 << TAIL_BITS),
+                                 in.tail_old | ((uint64_t)(fit < in.fit ? fit : in.fit) << TAIL_BITS));
     const bool full = failed || in.overflow;
     // an UNINITIALIZED key whose first bucket does not fit becomes FULL(0, 0) (:254)
     *hp = pack_handle(full ? H_FULL : H_READY, count, count == 0 ? 0 : prev);
@@ -177,27 +185,38 @@ __global__ void k_bucket_alloc_seq(BucketRef B, Layout lay, const uint64_t* __re
 template <typename V>
 __global__ void k_bucket_write(BucketRef B, const int64_t* __restrict__ slots, const uint32_t* __restrict__ rank,
                                const V* __restrict__ vals, uint64_t n, uint8_t* __restrict__ status) {
+  // growth prefix sums in shared memory when the table is short (a binary search per
+  // value over global memory dominated this pass)
+  constexpr uint32_t SM_SUMS = 2048;
+  __shared__ uint64_t s_sums[SM_SUMS];
+  Growth gr = B.gr;
+  if (gr.m <= SM_SUMS) {
+    for (uint32_t i = threadIdx.x; i < gr.m; i += blockDim.x) s_sums[i] = __ldg(B.gr.sums + i);
+    __syncthreads();
+    gr.sums = s_sums;
+  }
   const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
   V* arena = static_cast<V*>(B.arena);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const int64_t s = slots[i];
     if (s < 0) continue;  // INVALID_KEY / TABLE_FULL from the key store stay
-    const BucketInfo in = B.info[s];
+    const ulonglong2 wi = B.winfo[s];  // 16 B: region | c0, tail_old | fit
+    const uint64_t region = wi.x & TAIL_MAX, tail_old = wi.y & TAIL_MAX;
+    const uint32_t c0 = (uint32_t)(wi.x >> TAIL_BITS), fit = (uint32_t)(wi.y >> TAIL_BITS);
     const uint32_t r = rank[i];
-    if (r >= in.fit) {
+    if (r >= fit) {
       status[i] = ST_OOM;
       continue;
     }
-    const uint64_t v = (uint64_t)in.c0 + r;  // value index in the key's chain
-    const uint64_t b = B.gr.buckets_for(v + 1) - 1;
-    const uint64_t within = v - B.gr.before(b);
+    const uint64_t v = (uint64_t)c0 + r;  // value index in the key's chain
+    const uint64_t b = gr.buckets_for_gen(v + 1) - 1;
+    const uint64_t within = v - gr.before_gen(b);
     uint64_t base;
-    const uint64_t b_new0 = B.gr.buckets_for(in.c0);
-    if (in.c0 > 0 && b + 1 == b_new0) {
-      base = in.tail_old;  // room left in the old tail bucket (:266-276)
+    const uint64_t b_new0 = gr.buckets_for_gen(c0);
+    if (c0 > 0 && b + 1 == b_new0) {
+      base = tail_old;  // room left in the old tail bucket (:266-276)
     } else {
-      base = in.region + (B.gr.before(b) - B.gr.before(b_new0)) + (b - b_new0) -
-             ((b_new0 == 0 && b > 0) ? 1 : 0);
+      base = region + (gr.before_gen(b) - gr.before_gen(b_new0)) + (b - b_new0) - ((b_new0 == 0 && b > 0) ? 1 : 0);
     }
     arena[base + (b > 0 ? 1 : 0) + within] = ld_stream(vals + i);
     status[i] = ST_INSERTED;

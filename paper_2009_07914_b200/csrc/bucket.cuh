@@ -31,6 +31,18 @@ struct Growth {            // exact growth geometry, host-computed (GrowthPolicy
   }
   // capacity_of(b): values held by buckets 0..b-1
   __device__ __forceinline__ uint64_t before(uint64_t b) const { return b ? __ldg(sums + b - 1) : 0; }
+  // the same through a generic pointer (sums may point to shared memory)
+  __device__ __forceinline__ uint64_t buckets_for_gen(uint64_t count) const {
+    if (count == 0) return 0;
+    uint64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (sums[mid] < count) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo + 1;
+  }
+  __device__ __forceinline__ uint64_t before_gen(uint64_t b) const { return b ? sums[b - 1] : 0; }
   __device__ __forceinline__ uint64_t size(uint64_t b) const { return __ldg(sizes + b); }
   // arena cells of buckets [b0, b1] (bucket b > 0 spends one cell on the prev link)
   __device__ __forceinline__ uint64_t cells(uint64_t b0, uint64_t b1) const {
@@ -56,6 +68,7 @@ struct BucketRef {
   unsigned long long* bump;
   uint32_t* bcnt;          // per slot batch counts, zero at rest
   BucketInfo* info;
+  ulonglong2* winfo;       // per slot, final for the batch: {region | c0 << 42, tail_old | fit << 42}
   unsigned long long* first_fail;
   Growth gr;
 };
