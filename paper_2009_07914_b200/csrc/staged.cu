@@ -308,14 +308,10 @@ __global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, cons
   }
   __syncthreads();
   const uint32_t hv = hist[threadIdx.x];
+  // the run's global position: the atomic's round trip overlaps the bucketing below
+  const uint32_t gb = hv ? atomicAdd(&cursor[g.cbase + threadIdx.x], hv) : 0u;
   const uint32_t bo = block_excl_scan(hv, wt);
   boff[threadIdx.x] = bo;
-  const uint32_t gb = hv ? atomicAdd(&cursor[g.cbase + threadIdx.x], hv) : 0u;
-  gbase[threadIdx.x] = gb;
-  if (th && threadIdx.x < nb) {
-    th[(uint64_t)t * nb + threadIdx.x] = (uint16_t)hv;
-    tg[(uint64_t)t * nb + threadIdx.x] = gb;
-  }
   __syncthreads();
 #pragma unroll
   for (int it = 0; it < PI; ++it) {
@@ -330,6 +326,11 @@ __global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, cons
     sD[j] = (uint16_t)b;
     if (L == 2) sL[j] = (uint16_t)(d[it] >> 16);
     if (inv) inv[g.pos0 + li] = (uint16_t)j;
+  }
+  gbase[threadIdx.x] = gb;
+  if (th && threadIdx.x < nb) {
+    th[(uint64_t)t * nb + threadIdx.x] = (uint16_t)hv;
+    tg[(uint64_t)t * nb + threadIdx.x] = gb;
   }
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < g.cnt; j += PT) {
