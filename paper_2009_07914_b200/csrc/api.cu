@@ -595,7 +595,7 @@ int ch_multi_insert(ch_table* t, const void* keys, const void* vals, uint64_t n,
   if (t->cfg.kind != CH_MULTI) return fail(CH_EINVAL, "ch_multi_insert needs a multi-value table");
   if (n && (!keys || !vals || !status)) return fail(CH_EINVAL, "null buffer");
   Ordered o(t, stream);
-  if (n >= 4096 && t->group_mode != 1) {  // grouped: one sequence walk per distinct key (mgroup.cu)
+  if (n >= 4096 && n < (1ull << 31) && t->group_mode != 1) {  // grouped: one walk per distinct key (mgroup.cu)
     Scratch sc(o.s);
     const size_t bytes = mgroup_scratch_bytes(n, t->ts.kbytes, t->ts.vbytes);
     void* p = sc.get(bytes);

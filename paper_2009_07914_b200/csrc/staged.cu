@@ -45,7 +45,7 @@ constexpr int ST_S2 = 8;                   // regions per super-region = 2^ST_S2
 constexpr int PT = 512, PI = 8;            // partition CTA: threads x items
 constexpr uint32_t PTILE = (uint32_t)PT * PI;
 constexpr uint32_t PBINS = 512;
-constexpr int RT = 256;                    // region CTA threads
+constexpr int RT = 512;                    // region CTA threads
 constexpr uint32_t ST_MAX_REGIONS = 51200; // count histogram in shared memory (200 KiB)
 
 // Start slot of window wj (0 or 1) of key's COPS sequence: h, or h + step mod c
@@ -623,8 +623,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
           return true;
         }
         occ += 1;
-        claimed_any = true;
-        status[ri] = ST_INSERTED;
+        claimed_any = true;  // status: INSERTED is pre-set (staged_insert)
       }
     } else {
       const bool hit = c == k;
@@ -957,6 +956,7 @@ int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
   const bool r2 = g_round2;
   const StBufs b = st_carve(p, n, true, r2, scratch, &total);
   int rc = cuda_check(cudaMemsetAsync(b.dcount, 0, 24, lc.stream), "memset");  // lists A, B; exceptions
+  if (!rc) rc = cuda_check(cudaMemsetAsync(b.rf, ST_INSERTED, n, lc.stream), "memset");  // exceptions overwrite
   unsigned long long* exc = b.dcount + 2;
   if (!rc)
     rc = st_forward<1>(lc, T, p, b.r1, (const uint32_t*)keys, (const uint32_t*)vals, nullptr, nullptr, n, nullptr, 0,
