@@ -92,23 +92,86 @@ def make_keys(rank: int, n: int, world: int, device):
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
+    """Samples SM clocks and clock-event (throttle) reasons DURING the timed region.
+
+    NVML from a background thread every 5 ms (the timed region is ~0.1 s, shorter than
+    nvidia-smi's own start-up); `nvidia-smi -lms` only if NVML is unavailable.  __enter__
+    returns after the first sample so the region is covered from its start."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.samples = []          # (sm_mhz, max_mhz, set(reasons))
+        self.source = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._handle = self._nvml_handle(pynvml, device)
+            self._nvml = pynvml
+            self._bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                          pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+            self._max = float(pynvml.nvmlDeviceGetMaxClockInfo(self._handle, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self._nvml = None
+
+    @staticmethod
+    def _nvml_handle(pynvml, device: int):
+        try:   # CUDA ordinal -> NVML handle through the PCI bus id (CUDA_VISIBLE_DEVICES-proof)
+            import torch
+            pr = torch.cuda.get_device_properties(device)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml.nvmlDeviceGetHandleByIndex(device)
+
+    def _sample_nvml(self):
+        nv = self._nvml
+        sm = float(nv.nvmlDeviceGetClockInfo(self._handle, nv.NVML_CLOCK_SM))
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._handle)
+        return sm, self._max, {n for n, b in zip(self.NAMES, self._bits) if bits & b}
+
+    def _loop(self):
+        import time as _t
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._sample_nvml())
+            except Exception:
+                pass
+            self._first.set()
+            _t.sleep(0.005)
 
     def __enter__(self):
+        import threading
+        if self._nvml is not None:
+            self.source = "nvml"
+            self._stop, self._first = threading.Event(), threading.Event()
+            self._thread = threading.Thread(target=self._loop, daemon=True)
+            self._thread.start()
+            self._first.wait(5)
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi"
+            self._first_line = self.proc.stdout.readline()   # wait until sampling is live
         except OSError:
             self.proc = None
         return self
 
     def __exit__(self, *exc):
+        if self._nvml is not None:
+            self._stop.set()
+            self._thread.join(5)
+            try:
+                self.samples.append(self._sample_nvml())
+            except Exception:
+                pass
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -116,27 +179,23 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
-        else:
-            self.lines = []
+            for ln in [self._first_line] + out.splitlines():
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    sm, mx = float(parts[0]), float(parts[1])
+                except ValueError:
+                    continue
+                self.samples.append((sm, mx, {n for n, f in zip(self.NAMES, parts[2:6])
+                                              if f.lower().startswith("active")}))
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], 0.0, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for name, flag in zip(names, parts[2:6]):
-                if flag.lower().startswith("active"):
-                    reasons.add(name)
+        sm = [s[0] for s in self.samples]
+        mx = max((s[1] for s in self.samples), default=0.0)
+        reasons = set().union(*(s[2] for s in self.samples)) if self.samples else set()
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
 
 
 def measured_peak() -> tuple[float, str]:

@@ -308,6 +308,9 @@ def all_to_all_segments(send: torch.Tensor, send_counts: list[int], group=None):
     gloo on CPU).  Returns (recv, recv_counts)."""
     import torch.distributed as dist
     world = dist.get_world_size(group)
+    home = send.device
+    if _host_staged(send, group):
+        send = send.cpu()
     sc = torch.tensor(send_counts, dtype=torch.int64, device=send.device)
     rc = torch.empty(world, dtype=torch.int64, device=send.device)
     dist.all_to_all_single(rc, sc, group=group)
@@ -315,16 +318,27 @@ def all_to_all_segments(send: torch.Tensor, send_counts: list[int], group=None):
     recv = torch.empty(sum(recv_counts), dtype=send.dtype, device=send.device)
     dist.all_to_all_single(recv, send, output_split_sizes=recv_counts, input_split_sizes=list(send_counts),
                            group=group)
-    return recv, recv_counts
+    return recv.to(home), recv_counts
+
+
+def _host_staged(t: torch.Tensor, group) -> bool:
+    """gloo has no device all_to_all: device tensors cross it through host memory.
+    Used by the world-size-2 tests that run two ranks on one GPU; NCCL exchanges
+    device memory directly."""
+    import torch.distributed as dist
+    return t.is_cuda and dist.get_backend(group) == "gloo"
 
 
 def all_to_all_back(send: torch.Tensor, counts_in: list[int], counts_out: list[int], group=None) -> torch.Tensor:
     """Reverse exchange with known split sizes (results travel back to the requesters)."""
     import torch.distributed as dist
+    home = send.device
+    if _host_staged(send, group):
+        send = send.cpu()
     recv = torch.empty(sum(counts_out), dtype=send.dtype, device=send.device)
     dist.all_to_all_single(recv, send, output_split_sizes=list(counts_out), input_split_sizes=list(counts_in),
                            group=group)
-    return recv
+    return recv.to(home)
 
 
 class ShardedTable:

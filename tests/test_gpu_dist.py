@@ -146,3 +146,55 @@ def test_sharded_table_single_rank_nccl():
         assert f.cpu().bool().all() and (v.cpu() == keys.cpu() * 3).all()
     finally:
         dist.destroy_process_group()
+
+
+def _sharded_worker(rank, world, port, q):
+    """One rank of a 2-rank ShardedTable job on cuda:0 (gloo exchange staged through host
+    memory; NCCL refuses two ranks on one GPU).  The data path (split -> exchange -> local
+    insert/retrieve -> exchange back -> scatter) is the one bench.py runs under torchrun."""
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        n, shared = 150_000, 20_000
+        own = torch.arange(1, n + 1, dtype=torch.int64) + rank * n       # disjoint per rank
+        common = torch.arange(10 * n, 10 * n + shared, dtype=torch.int64)  # inserted by both
+        keys = torch.cat([own, common]).to(torch.int32).cuda()
+        keys = keys[torch.randperm(keys.numel(), device="cuda")]
+        table = SingleValueHashTable(1 << 19, layout="packed", key_bits=32, value_bits=32)
+        st = ShardedTable(table)
+        status = st.insert_device(keys, keys * 3).cpu()
+        ins = torch.tensor([int((status == 0).sum()), int((status == 1).sum()), table.occupied])
+        dist.all_reduce(ins)
+        # every rank asks for all keys (its own, the peer's, the shared ones, and misses)
+        allk = torch.arange(1, world * n + 1, dtype=torch.int32)
+        q_keys = torch.cat([allk, common.to(torch.int32), torch.arange(20 * n, 20 * n + 999, dtype=torch.int32)])
+        v, f = st.retrieve_device(q_keys.cuda())
+        v, f = v.cpu(), f.cpu().bool()
+        hit = q_keys.numel() - 999
+        ok = bool(f[:hit].all()) and not bool(f[hit:].any()) and bool((v[:hit] == q_keys[:hit] * 3).all())
+        q.put((rank, ok, ins.tolist()))
+    except Exception as e:  # surface the failure to the parent
+        q.put((rank, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_table_world2_one_gpu():
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(60)
+    assert all(ok for _, ok, _ in res), res
+    inserted, dup, size = res[0][2]
+    assert inserted == 2 * 150_000 + 20_000 == size     # each shared key lands once
+    assert dup == 20_000                                 # ...and its second copy is DUPLICATE
