@@ -430,7 +430,6 @@ __global__ void __launch_bounds__(PT) k_st_gather(uint64_t n, const uint64_t* __
 // the device-counted list in batches (one global atomic per flush: a per-warp
 // atomic on one counter serialised the whole pass).
 constexpr uint32_t DBUF = 256;    // deferred entries buffered per CTA
-constexpr uint32_t SEG = 2048;    // keys staged per segment
 constexpr uint32_t STEP = 8;      // slots one key examines per round
 constexpr uint32_t TILE_PAD = 8;  // a step may read up to STEP-1 slots past its window
 
@@ -496,33 +495,26 @@ __device__ __forceinline__ uint64_t lds64(const uint64_t* p) {
   return v;
 }
 
-// warp-aggregated append of e to a shared-memory queue (all lanes call it)
-__device__ __forceinline__ void queue_push(bool push, uint16_t e, uint16_t* q, uint32_t* qn) {
-  const unsigned mk = __ballot_sync(0xffffffffu, push);
-  if (!mk) return;
-  const int lane = threadIdx.x & 31, leader = __ffs(mk) - 1;
-  uint32_t b = 0;
-  if (lane == leader) b = atomicAdd(qn, (uint32_t)__popc(mk));
-  b = __shfl_sync(0xffffffffu, b, leader);
-  if (push) q[b + __popc(mk & ((1u << lane) - 1u))] = e;
-}
-
 // Region pass.  Results are written at the key's region-ordered position (the
 // gather passes return them to the caller's order): MODE 0 insert the status,
 // MODE 1 lookup the value and found flag.
 //
-// The region's keys are staged a segment at a time and resolved in ROUNDS: in
-// every round each pending key examines the next STEP slots of window 0 (one
-// thread per key, the same work for every lane), and keys that are still open
-// -- nothing decisive in those slots, or an insert that lost its CAS to
-// another key of the round -- are compacted into the next round's queue.  A
-// thread-per-key loop over the whole window ran at ~7 of 32 active lanes (the
-// warp waited on its longest probe; profiles/r01_region_v3).
+// Every lane of a warp holds one open key and advances it STEP slots of window 0
+// per iteration (the same work for every lane); a lane whose key resolved takes
+// the next one from the warp's key chunks (32 keys loaded coalesced into
+// registers, the following chunk already in flight, handed out with shuffles;
+// chunks come from a per-region counter, so warps balance themselves).  No
+// barrier between the tile load and the write-back: a staged-segment version
+// with rounds and a shared-memory queue spent 26% of its stalls at segment
+// barriers and 10% of its instructions on the queue (profiles/r01_ncu_staged_probe).
 // R2 (round 2): the keys are round 1's deferred ones, probed in window 1, and each
 // carries the position its result belongs to (pos).  Deferrals go to DA when the
 // COPS kernel must re-examine the window (start crossing the region end, a
 // tombstone before the first empty) and to DB when the window is full (round 1:
 // those are round 2's input; round 2: DB == DA, the COPS kernel's list).
+constexpr uint32_t DBUF_B = 1024;  // window-full deferrals buffered per region (~4.6% of ~7.8K keys)
+constexpr uint32_t NONE = 0xffffffffu;
+
 template <int MODE, bool R2>
 __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* __restrict__ foff,
                                                     const uint32_t* __restrict__ keys,
@@ -537,19 +529,15 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
   constexpr uint32_t OW = R2 ? WINDOW : 0u;  // sequence offset of the window probed here
   extern __shared__ __align__(128) unsigned char dsm[];
   uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
-  uint32_t* s_key = reinterpret_cast<uint32_t*>(tile + ST_R + HALO + TILE_PAD);
-  uint32_t* s_val = s_key + SEG;  // insert only
-  uint32_t* s_pos = s_val + (INS ? SEG : 0);  // round 2 only
-  uint16_t* s_lo = reinterpret_cast<uint16_t*>(s_pos + (R2 ? SEG : 0));
-  uint16_t* s_q0 = s_lo + SEG;  // keys open after round 0: i << 5 | o
-  __shared__ DeferBuf<INS, DBUF> B;   // -> DB
-  __shared__ DeferBuf<INS, DBUF> BA;  // -> DA
-  __shared__ uint32_t s_qn[2];
+  __shared__ DeferBuf<INS, DBUF_B> B;  // -> DB
+  __shared__ DeferBuf<INS, DBUF> BA;   // -> DA
+  __shared__ uint32_t s_next;
   __shared__ __align__(8) uint64_t bar;
   __shared__ int dirty;
   const uint32_t f = blockIdx.x;
   const uint64_t k0 = foff[f], k1 = foff[f + 1];
   if (k0 == k1) return;  // no key starts in this region
+  const uint32_t m = (uint32_t)(k1 - k0);
   const uint64_t rbase = (uint64_t)f << ST_LOG_R;
   const uint32_t len = (uint32_t)((T.c - rbase) < ST_R ? (T.c - rbase) : ST_R);
   uint64_t* slots = static_cast<uint64_t*>(T.slots);
@@ -557,6 +545,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
     dirty = 0;
     B.n = 0;
     BA.n = 0;
+    s_next = 0;
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, (len + HALO) * 8u);
     bulk_load(tile, slots + rbase, len * 8u, &bar);
@@ -568,17 +557,14 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
   __syncthreads();  // the mbarrier is initialised before anyone waits on it
   const uint32_t e = (uint32_t)T.e, t = (uint32_t)T.t;
   const uint32_t ug = (uint32_t)g;
+  const uint32_t lane = threadIdx.x & 31u;
   long long ops = 0, att = 0, win = 0, occ = 0, ndef = 0, nexc = 0;
-  bool claimed_any = false, waited = false;
+  bool claimed_any = false;
+  const bool adj = t + 1u == e;  // default sentinels: "free" is one subtract and compare, (c - t) <= 1
 
-  // Sentinel test: with the default sentinels (t = e - 1) "free" is one subtract
-  // and compare, (c - t) <= 1.
-  const bool adj = t + 1u == e;
-  // one probe step of segment key i from in-window offset o (updated); returns true
-  // when the key stays open (nothing decisive in these slots, or a lost claim)
-  auto step = [&](uint64_t s0, uint32_t i, uint32_t& o) -> bool {
-    const uint32_t k = s_key[i], lo = s_lo[i];
-    const uint32_t ri = R2 ? s_pos[i] : (uint32_t)(s0 + i);  // where the key's result goes
+  // one probe step of key k from in-window offset o (updated); true while the key
+  // stays open (nothing decisive in these slots, or a lost claim)
+  auto step = [&](uint32_t k, uint32_t v, uint32_t lo, uint32_t ri, uint32_t& o) -> bool {
     uint64_t w[STEP];
 #pragma unroll
     for (int u = 0; u < (int)STEP; ++u) w[u] = INS ? lds64(tile + lo + o + u) : tile[lo + o + u];
@@ -586,18 +572,18 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
     const uint32_t room = WINDOW - o;  // slots left in the window
     uint32_t u = STEP;
 #pragma unroll
-    for (int v = (int)STEP - 1; v >= 0; --v) {
-      const uint32_t c = (uint32_t)w[v];
+    for (int q = (int)STEP - 1; q >= 0; --q) {
+      const uint32_t c = (uint32_t)w[q];
       bool d;
       if (INS) d = (c == k) | (adj ? (c - t) <= 1u : ((c == e) | (c == t)));
       else d = (c == k) | (c == e);  // lookups pass tombstones
-      u = (d && (uint32_t)v < room) ? (uint32_t)v : u;
+      u = (d && (uint32_t)q < room) ? (uint32_t)q : u;
     }
     if (u == STEP) {
       o += STEP;
       if (o < WINDOW) return true;
       // the window holds neither the key nor a free cell: resume at the next one
-      defer_push(B, DB, k, INS ? s_val[i] : 0u, ri, OW + WINDOW);
+      defer_push(B, DB, k, v, ri, OW + WINDOW);
       ndef += 1;
       return false;
     }
@@ -609,13 +595,13 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
         status[ri] = ST_DUPLICATE;
         nexc += 1;
       } else if (c == t) {  // tombstone first: the deferred-claim rule (:201-223), COPS kernel
-        defer_push(BA, DA, k, s_val[i], ri, OW);
+        defer_push(BA, DA, k, v, ri, OW);
         ndef += 1;
         return false;
       } else {
         bool won = false;
         if (c == e) {
-          const unsigned long long want = ((unsigned long long)s_val[i] << 32) | k;
+          const unsigned long long want = ((unsigned long long)v << 32) | k;
           won = atomicCAS((unsigned long long*)(tile + lo + o), (unsigned long long)wd, want) == wd;
         }
         if (!won) {  // another key took it: re-read from this slot (single_table.py:232-233)
@@ -636,96 +622,95 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
     return false;
   };
 
-  for (uint64_t s0 = k0; s0 < k1; s0 += SEG) {
-    const uint32_t m = (uint32_t)((k1 - s0) < SEG ? (k1 - s0) : SEG);
-    if (threadIdx.x == 0) {
-      s_qn[0] = 0;
-      s_qn[1] = 0;
+  // key chunks: 32 consecutive keys of the region's list, one per lane
+  auto grab = [&]() -> uint32_t {
+    uint32_t b = 0;
+    if (lane == 0) b = atomicAdd(&s_next, 32u);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    return b < m ? b : NONE;
+  };
+  uint32_t ck = e, cv = 0, cp = 0, cl = 0, nk = e, nv = 0, np = 0, nl = 0;
+  auto fetch = [&](uint32_t b, uint32_t& kk, uint32_t& vv, uint32_t& pp, uint32_t& ll) {
+    const uint32_t i = b + lane;
+    if (b != NONE && i < m) {
+      kk = __ldcs(keys + k0 + i);
+      ll = __ldcs(los + k0 + i);
+      if (INS) vv = __ldcs(vals + k0 + i);
+      if (R2) pp = __ldcs(pos + k0 + i);
     }
-    // stage the segment (all loads in flight): keys, window starts (+ values)
-    constexpr int PER = SEG / RT;
-    uint32_t kk[PER], vv[PER], pp[PER];
-    uint16_t ll[PER];
-#pragma unroll
-    for (int r = 0; r < PER; ++r) {
-      const uint32_t i = (uint32_t)r * RT + threadIdx.x;
-      kk[r] = i < m ? __ldcs(keys + s0 + i) : e;
-      ll[r] = i < m ? __ldcs(los + s0 + i) : (uint16_t)0;
-      if (INS) vv[r] = i < m ? __ldcs(vals + s0 + i) : 0u;
-      if (R2) pp[r] = i < m ? __ldcs(pos + s0 + i) : 0u;
-    }
-#pragma unroll
-    for (int r = 0; r < PER; ++r) {
-      const uint32_t i = (uint32_t)r * RT + threadIdx.x;
-      s_key[i] = kk[r];
-      s_lo[i] = ll[r];
-      if (INS) s_val[i] = vv[r];
-      if (R2) s_pos[i] = pp[r];
-    }
-    if (!waited) {
-      mbar_wait(&bar, 0);
-      waited = true;
-    }
-    __syncthreads();
-    // round 0 over the staged segment
-    for (uint32_t base = 0; base < m; base += RT) {
-      const uint32_t i = base + threadIdx.x;
-      bool push = false;
-      uint16_t pe = 0;
-      if (i < m) {
-        const uint32_t k = s_key[i];
+  };
+  uint32_t cbase = grab();
+  fetch(cbase, ck, cv, cp, cl);
+  uint32_t nbase = cbase == NONE ? NONE : grab();
+  fetch(nbase, nk, nv, np, nl);
+  uint32_t ptr = 0;  // entries of the current chunk handed out
+  mbar_wait(&bar, 0);
+
+  bool act = false;
+  uint32_t k = 0, v = 0, lo = 0, ri = 0, o = 0;
+  for (;;) {
+    const unsigned need = __ballot_sync(0xffffffffu, !act);
+    if (need && cbase != NONE) {
+      const uint32_t take = ptr + __popc(need & ((1u << lane) - 1u));  // < 64
+      const uint32_t src = take & 31u;
+      const bool fromc = take < 32u;
+      // (the source lane cannot choose the chunk: it does not know the taker's take)
+      auto pick = [&](uint32_t cur, uint32_t nxt) {
+        const uint32_t a = __shfl_sync(0xffffffffu, cur, src), b = __shfl_sync(0xffffffffu, nxt, src);
+        return fromc ? a : b;
+      };
+      const uint32_t xk = pick(ck, nk), xl = pick(cl, nl);
+      const uint32_t xv = INS ? pick(cv, nv) : 0u, xp = R2 ? pick(cp, np) : 0u;
+      const uint32_t tb = fromc ? cbase : nbase;
+      const bool got = !act && tb != NONE && tb + src < m;
+      ptr += __popc(need);
+      if (ptr >= 32u) {  // current chunk used up: the next one moves in, another is fetched
+        ptr -= 32u;
+        cbase = nbase;
+        ck = nk, cv = nv, cp = np, cl = nl;
+        nbase = cbase == NONE ? NONE : grab();
+        fetch(nbase, nk, nv, np, nl);
+      }
+      if (got) {
+        k = xk, v = xv, lo = xl, o = 0;
+        ri = R2 ? xp : (uint32_t)(k0 + tb + src);
         if (k == e || k == t) {  // sentinels are never stored (single_table.py:369-370, 391-393)
           if (INS) {
-            status[s0 + i] = ST_INVALID;
+            status[ri] = ST_INVALID;
             nexc += 1;
           } else {
-            res_val[s0 + i] = 0;
-            res_flag[s0 + i] = 0;
+            res_val[ri] = 0;
+            res_flag[ri] = 0;
             ops += 1;  // retrieve_bulk counts every query (:403)
           }
-        } else if (INS && s_lo[i] + WINDOW > len) {  // the window leaves the staged region
-          defer_push(BA, DA, k, s_val[i], R2 ? s_pos[i] : (uint32_t)(s0 + i), OW);
+        } else if (INS && lo + WINDOW > len) {  // the window leaves the staged region
+          defer_push(BA, DA, k, v, ri, OW);
           ndef += 1;
         } else {
-          uint32_t o = 0;
-          push = step(s0, i, o);
-          pe = (uint16_t)(i << 5 | o);
+          act = true;
         }
       }
-      queue_push(push, pe, s_q0, &s_qn[0]);
     }
-    // the keys still open after round 0: every thread takes one from the queue and
-    // finishes it, step by step, then takes the next (no barrier between steps)
-    __syncthreads();
-    const uint32_t qn = s_qn[0];
-    for (;;) {
-      const uint32_t j = atomicAdd(&s_qn[1], 1u);
-      if (j >= qn) break;
-      const uint32_t ent = s_q0[j];
-      const uint32_t i = ent >> 5;
-      uint32_t o = ent & 31u;
-      while (step(s0, i, o)) {
-      }
-    }
-    defer_flush(B, DB, s0 + SEG >= k1);  // syncs: the segment buffers are free again
-    defer_flush(BA, DA, s0 + SEG >= k1);
+    if (act) act = step(k, v, lo, ri, o);
+    if (cbase == NONE && !__any_sync(0xffffffffu, act)) break;
   }
+  defer_flush(B, DB, true);  // syncs
+  defer_flush(BA, DA, true);
   if (INS) {
     if (claimed_any) dirty = 1;
     fence_smem_to_async();
     __syncthreads();
     if (threadIdx.x == 0 && dirty) bulk_store_wait(slots + rbase, tile, len * 8u);
   }
-  const long long v[6] = {ops, att, win, occ, nexc, ndef};
+  const long long cv6[6] = {ops, att, win, occ, nexc, ndef};
   long long* const dst[6] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
                              &T.ctr->occupied, INS ? (long long*)exc : nullptr, (long long*)&T.ctr->deferred};
-  cta_add<6>(v, dst);
+  cta_add<6>(cv6, dst);
 }
 
 template <int MODE, bool R2>
 constexpr size_t probe_smem() {
-  return (size_t)(ST_R + (MODE == 0 ? 0 : ST_HALO) + TILE_PAD) * 8 +
-         (size_t)SEG * (4 + (MODE == 0 ? 4 : 0) + (R2 ? 4 : 0) + 2 + 2);
+  return (size_t)(ST_R + (MODE == 0 ? 0 : ST_HALO) + TILE_PAD) * 8;
 }
 
 // ------------------------------------------------------------- host side
