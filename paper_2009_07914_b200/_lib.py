@@ -11,7 +11,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcoophash_b200.so")
+# CH_LIB_PATH: an alternative build of the same library (A/B measurements, tools/ab.sh)
+LIB_PATH = os.environ.get("CH_LIB_PATH") or os.path.join(_HERE, "libcoophash_b200.so")
 
 CH_OK, CH_EINVAL, CH_ENOMEM, CH_EIO, CH_ETIMEDOUT = 0, -22, -12, -5, -110
 CH_SINGLE, CH_MULTI, CH_BUCKET = 0, 1, 2

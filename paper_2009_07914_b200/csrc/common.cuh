@@ -71,6 +71,14 @@ struct FastMod {
     uint64_t r = x - q * d;
     return r >= d ? r - d : r;
   }
+  // d < 2^31 (and >= 2): the remainder before the correction is below 2d < 2^32,
+  // so it is exact in the low words (one 32-bit multiply instead of a 64-bit one)
+  __device__ __forceinline__ uint32_t mod31(uint64_t x) const {
+    const uint32_t q = (uint32_t)__umul64hi(x, m);
+    const uint32_t r = (uint32_t)x - q * (uint32_t)d;
+    return r >= (uint32_t)d ? r - (uint32_t)d : r;
+  }
+  __device__ __forceinline__ uint64_t mod_any(uint64_t x) const { return (d >> 31) ? mod(x) : (uint64_t)mod31(x); }
 };
 
 // Everything a kernel needs to walk a table.  Passed by value.
@@ -92,8 +100,8 @@ struct ProbeStart {
 
 __device__ __forceinline__ ProbeStart probe_start(const TableRef& T, uint64_t key) {
   ProbeStart s;
-  s.h = T.modc.mod(mix64(key));  // HashFn(0).value(key) % c
-  s.step = T.p == 2 ? (uint64_t)WINDOW : (uint64_t)WINDOW * (1 + T.modpm1.mod(mix64(STEP_SEED ^ key)));
+  s.h = T.modc.mod_any(mix64(key));  // HashFn(0).value(key) % c
+  s.step = T.p == 2 ? (uint64_t)WINDOW : (uint64_t)WINDOW * (1 + T.modpm1.mod_any(mix64(STEP_SEED ^ key)));
   return s;
 }
 

@@ -26,7 +26,7 @@ constexpr uint32_t LOC_MAX_REGIONS = 1024;
 
 template <typename K>
 __device__ __forceinline__ uint32_t region_of(const TableRef& T, K key, int shift) {
-  return (uint32_t)(T.modc.mod(mix64((uint64_t)key)) >> shift);
+  return (uint32_t)(T.modc.mod_any(mix64((uint64_t)key)) >> shift);
 }
 
 // hist[r * tiles + tile] = keys of the tile whose first window starts in region r

@@ -47,13 +47,14 @@ constexpr uint32_t PTILE = (uint32_t)PT * PI;
 constexpr uint32_t PBINS = 512;
 constexpr int RT = 512;                    // region CTA threads
 constexpr uint32_t ST_MAX_REGIONS = 51200; // count histogram in shared memory (200 KiB)
+static_assert((ST_MAX_REGIONS >> ST_S2) <= (uint32_t)PT, "tile_super: one super-region per thread");
 
 // Start slot of window wj (0 or 1) of key's COPS sequence: h, or h + step mod c
 // (probing.py:202-220; step = 32 (1 + stephash mod (p-1)), p = 2 -> 32).  c < 2^32.
 __device__ __forceinline__ uint32_t window_start(const TableRef& T, uint32_t key, int wj) {
-  uint64_t ws = T.modc.mod(mix64((uint64_t)key));
+  uint64_t ws = T.modc.mod_any(mix64((uint64_t)key));
   if (wj) {
-    ws += T.p == 2 ? (uint64_t)WINDOW : (uint64_t)WINDOW * (1 + T.modpm1.mod(mix64(STEP_SEED ^ (uint64_t)key)));
+    ws += T.p == 2 ? (uint64_t)WINDOW : (uint64_t)WINDOW * (1 + T.modpm1.mod_any(mix64(STEP_SEED ^ (uint64_t)key)));
     if (ws >= T.c) ws -= T.c;
   }
   return (uint32_t)ws;
@@ -188,6 +189,8 @@ __global__ void __launch_bounds__(PT) k_st_plan(const uint64_t* __restrict__ fof
 // Geometry of partition tile `t` of level L.  Level 1 tiles are the input cut in
 // PTILE pieces; level 2 tiles are each super-region (input: level-1 order) cut in
 // PTILE pieces.  Returns false for CTAs past the last tile.
+constexpr uint32_t NO_SUPER = 0xffffffffu;
+
 struct TileGeo {
   uint64_t pos0;   // first element (position in this level's input order)
   uint32_t cnt;    // elements
@@ -196,8 +199,7 @@ struct TileGeo {
 
 template <int L>
 __device__ __forceinline__ bool tile_geo(uint32_t t, uint64_t n, const uint64_t* __restrict__ foff,
-                                         const uint32_t* tstart, uint32_t supers, uint32_t regions,
-                                         TileGeo& g) {
+                                         const uint32_t* sup, uint32_t regions, TileGeo& g) {
   if (L == 1) {
     g.pos0 = (uint64_t)t * PTILE;
     if (g.pos0 >= n) return false;
@@ -205,20 +207,35 @@ __device__ __forceinline__ bool tile_geo(uint32_t t, uint64_t n, const uint64_t*
     g.cbase = 0;
     return true;
   }
-  if (t >= tstart[supers]) return false;
-  uint32_t lo = 0, hi = supers;  // last b with tstart[b] <= t (tstart: a shared-memory copy)
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (tstart[mid] <= t) lo = mid;
-    else hi = mid;
-  }
+  const uint32_t lo = sup[0];  // the tile's super-region and its first tile (tile_super)
+  if (lo == NO_SUPER) return false;
   const uint64_t r0 = (uint64_t)lo << ST_S2;
   const uint64_t r1 = ((uint64_t)(lo + 1) << ST_S2) < regions ? ((uint64_t)(lo + 1) << ST_S2) : regions;
   const uint64_t s = foff[r0], e = foff[r1];
-  g.pos0 = s + (uint64_t)(t - tstart[lo]) * PTILE;
+  g.pos0 = s + (uint64_t)(t - sup[1]) * PTILE;
   g.cnt = (uint32_t)((e - g.pos0) < PTILE ? (e - g.pos0) : PTILE);
   g.cbase = (uint32_t)r0;
   return true;
+}
+
+// Level 2: the super-region owning tile t (tstart[b] <= t < tstart[b + 1]), found by
+// the CTA in one compare per thread (a per-thread binary search was 7% of the
+// split's instructions); sup[0] = the super-region or NO_SUPER, sup[1] = its first tile.
+__device__ __forceinline__ void tile_super(uint32_t t, const uint32_t* __restrict__ tstart, uint32_t supers,
+                                           uint32_t* sup) {
+  // every load before the first branch: one L2 round trip (supers <= blockDim.x)
+  const uint32_t tot = tstart[supers];
+  const uint32_t i = threadIdx.x;
+  const uint32_t a = i < supers ? tstart[i] : 0u, b = i < supers ? tstart[i + 1] : 0u;
+  if (t >= tot) {  // past the last tile (CTA-uniform)
+    sup[0] = NO_SUPER;
+    return;
+  }
+  if (a <= t && t < b) {
+    sup[0] = i;
+    sup[1] = a;
+  }
+  __syncthreads();
 }
 
 // PT-thread exclusive scan of v (one value per thread); returns the prefix.
@@ -232,8 +249,15 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wt) {
   }
   if (lane == 31) wt[warp] = x;
   __syncthreads();
-  uint32_t before = 0;
-  for (int w = 0; w < warp; ++w) before += wt[w];
+  // warp totals scanned with shuffles (a per-thread loop over the warps was 5% of
+  // the split's instructions)
+  uint32_t y = lane < PT / 32 ? wt[lane] : 0u;
+#pragma unroll
+  for (int d = 1; d < PT / 32; d <<= 1) {
+    const uint32_t z = __shfl_up_sync(0xffffffffu, y, d);
+    if (lane >= d) y += z;
+  }
+  const uint32_t before = warp ? __shfl_sync(0xffffffffu, y, warp - 1) : 0u;
   return before + x - v;
 }
 
@@ -251,8 +275,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // round-1 position of a round-2 key, or of a lookup key in round 2 with NPAY=1
 // meaning the position).  Round 2 (wj = 1) partitions the deferred keys by their
 // window-1 start; its count lives on the device (n_dev) and it needs no inverse.
+#ifndef CH_AB_SPLIT_MINB
+#define CH_AB_SPLIT_MINB 3  // 3 CTAs per SM (<= 42 registers, small spills): 26.5 -> 27.1 G ops/s
+#endif
 template <int L, int NPAY>
-__global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, const uint64_t* __restrict__ foff,
+__global__ void __launch_bounds__(PT, CH_AB_SPLIT_MINB) k_st_split(TableRef T, uint64_t n, const uint64_t* __restrict__ foff,
                                                     const uint32_t* __restrict__ tstart, uint32_t supers,
                                                     uint32_t regions, uint32_t ntiles,
                                                     const uint32_t* __restrict__ kin,
@@ -279,13 +306,13 @@ __global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, cons
   __shared__ uint32_t hist[PBINS], boff[PBINS], gbase[PBINS];
   __shared__ uint32_t wt[PT / 32];
   const uint32_t t = blockIdx.x;
-  __shared__ uint32_t s_ts[L == 2 ? PBINS + 1 : 1];
+  __shared__ uint32_t s_sup[2];
   if (L == 2) {
-    for (uint32_t i = threadIdx.x; i <= supers; i += PT) s_ts[i] = tstart[i];
-    __syncthreads();
+    if (t >= ntiles) return;
+    tile_super(t, tstart, supers, s_sup);
   }
   TileGeo g;
-  if (t >= ntiles || !tile_geo<L>(t, n, foff, s_ts, supers, regions, g)) return;
+  if (t >= ntiles || !tile_geo<L>(t, n, foff, s_sup, regions, g)) return;
   hist[threadIdx.x] = 0;  // PBINS == PT
   uint32_t k[PI], v[PI], q[PI], w[PI], d[PI], r[PI];
 #pragma unroll
@@ -327,7 +354,7 @@ __global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, cons
     if (L == 2) sL[j] = (uint16_t)(d[it] >> 16);
     if (inv) inv[g.pos0 + li] = (uint16_t)j;
   }
-  gbase[threadIdx.x] = gb;
+  gbase[threadIdx.x] = gb - bo;  // run destination minus its tile offset (u32 wrap is fine)
   if (th && threadIdx.x < nb) {
     th[(uint64_t)t * nb + threadIdx.x] = (uint16_t)hv;
     tg[(uint64_t)t * nb + threadIdx.x] = gb;
@@ -335,7 +362,7 @@ __global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, cons
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < g.cnt; j += PT) {
     const uint32_t b = sD[j];
-    const uint32_t dst = gbase[b] + (j - boff[b]);
+    const uint32_t dst = gbase[b] + j;
     kout[dst] = sK[j];
     if (VALS) vout[dst] = sV[j];
     if (POS) pout[dst] = sP[j];
@@ -350,8 +377,11 @@ __global__ void __launch_bounds__(PT, 2) k_st_split(TableRef T, uint64_t n, cons
 // all loads in flight (consecutive slots of a run are consecutive addresses;
 // default caching: a sector is shared by the runs of neighbouring tiles).
 // VAL: u32 value + u8 flag, otherwise u8 only (insert status).
+#ifndef CH_AB_GATHER_MINB
+#define CH_AB_GATHER_MINB 3  // 3 CTAs per SM (<= 42 registers): 57-58 registers ran 2 and measured slower
+#endif
 template <int L, bool VAL>
-__global__ void __launch_bounds__(PT) k_st_gather(uint64_t n, const uint64_t* __restrict__ foff,
+__global__ void __launch_bounds__(PT, CH_AB_GATHER_MINB) k_st_gather(uint64_t n, const uint64_t* __restrict__ foff,
                                                   const uint32_t* __restrict__ tstart, uint32_t supers,
                                                   uint32_t regions, uint32_t ntiles,
                                                   const uint16_t* __restrict__ inv,
@@ -363,23 +393,50 @@ __global__ void __launch_bounds__(PT) k_st_gather(uint64_t n, const uint64_t* __
   __shared__ uint32_t sV[VAL ? PTILE : 1];
   __shared__ uint8_t sF[PTILE];
   __shared__ uint16_t sB[PTILE];
-  __shared__ uint32_t boff[PBINS], hist[PBINS], gsrc[PBINS];
+  __shared__ uint32_t gsrc[PBINS];
   __shared__ uint32_t wt[PT / 32];
   const uint32_t t = blockIdx.x;
-  __shared__ uint32_t s_ts[L == 2 ? PBINS + 1 : 1];
+  __shared__ uint32_t s_sup[2];
+  if (t >= ntiles) return;
+  // every status INSERTED (insert without exceptions): nothing to move back
+  const bool skip = !VAL && exc && *exc == 0;
+  // the run table depends on t only: in flight while the geometry resolves
+  const bool rt = !skip && threadIdx.x < nb;
+  const uint32_t hv = rt ? th[(uint64_t)t * nb + threadIdx.x] : 0u;
+  const uint32_t gs = rt ? tg[(uint64_t)t * nb + threadIdx.x] : 0u;
   if (L == 2) {
+    if (skip) return;  // level 1 writes the statuses
+#ifdef CH_AB_GATHER_BSEARCH
+    __shared__ uint32_t s_ts[PBINS + 1];
     for (uint32_t i = threadIdx.x; i <= supers; i += PT) s_ts[i] = tstart[i];
     __syncthreads();
+    if (t >= s_ts[supers]) {
+      s_sup[0] = NO_SUPER;
+    } else {
+      uint32_t lo = 0, hi = supers;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_ts[mid] <= t) lo = mid;
+        else hi = mid;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_sup[0] = lo;
+        s_sup[1] = s_ts[lo];
+      }
+    }
+    __syncthreads();
+#else
+    tile_super(t, tstart, supers, s_sup);
+#endif
   }
   TileGeo g;
-  if (t >= ntiles || !tile_geo<L>(t, n, foff, s_ts, supers, regions, g)) return;
-  if (!VAL && exc && *exc == 0) {  // every status is INSERTED: nothing to move back
+  if (t >= ntiles || !tile_geo<L>(t, n, foff, s_sup, regions, g)) return;
+  if (skip) {
     if (L == 1)
       for (uint32_t li = threadIdx.x; li < g.cnt; li += PT) dst_f[g.pos0 + li] = ST_INSERTED;
     return;
   }
-  const uint32_t hv = threadIdx.x < nb ? th[(uint64_t)t * nb + threadIdx.x] : 0u;
-  const uint32_t gs = threadIdx.x < nb ? tg[(uint64_t)t * nb + threadIdx.x] : 0u;
   uint16_t iv[PI];
 #pragma unroll
   for (int it = 0; it < PI; ++it) {  // the inverse ranks load alongside the run table
@@ -387,9 +444,7 @@ __global__ void __launch_bounds__(PT) k_st_gather(uint64_t n, const uint64_t* __
     iv[it] = li < g.cnt ? __ldcs(inv + g.pos0 + li) : (uint16_t)0;
   }
   const uint32_t bo = block_excl_scan(hv, wt);
-  hist[threadIdx.x] = hv;
-  boff[threadIdx.x] = bo;
-  gsrc[threadIdx.x] = gs;
+  gsrc[threadIdx.x] = gs - bo;  // run source minus its tile offset
   __syncthreads();
   for (uint32_t x = 0; x < hv; ++x) sB[bo + x] = (uint16_t)threadIdx.x;  // thread b: its run's slots
   __syncthreads();
@@ -400,7 +455,7 @@ __global__ void __launch_bounds__(PT) k_st_gather(uint64_t n, const uint64_t* __
     const uint32_t j = (uint32_t)it * PT + threadIdx.x;
     if (j < g.cnt) {
       const uint32_t b = sB[j];
-      const uint32_t src = gsrc[b] + (j - boff[b]);
+      const uint32_t src = gsrc[b] + j;
       if (VAL) v[it] = src_v[src];
       fl[it] = src_f[src];
     }
