@@ -485,7 +485,10 @@ __global__ void __launch_bounds__(PT, CH_AB_GATHER_MINB) k_st_gather(uint64_t n,
 // the device-counted list in batches (one global atomic per flush: a per-warp
 // atomic on one counter serialised the whole pass).
 constexpr uint32_t DBUF = 256;    // deferred entries buffered per CTA
-constexpr uint32_t STEP = 8;      // slots one key examines per round
+#ifndef CH_AB_STEP
+#define CH_AB_STEP 8
+#endif
+constexpr uint32_t STEP = CH_AB_STEP;  // slots one key examines per step
 constexpr uint32_t TILE_PAD = 8;  // a step may read up to STEP-1 slots past its window
 
 template <bool VALS, uint32_t CAP>
