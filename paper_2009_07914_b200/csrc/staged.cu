@@ -547,9 +547,9 @@ __device__ __forceinline__ void defer_flush(DeferBuf<VALS, CAP>& B, const DeferO
   __syncthreads();
 }
 
-__device__ __forceinline__ uint64_t lds64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_addr(p)) : "memory");
+__device__ __forceinline__ uint32_t lds32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
   return v;
 }
 
@@ -622,20 +622,25 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
 
   // one probe step of key k from in-window offset o (updated); true while the key
   // stays open (nothing decisive in these slots, or a lost claim)
+  // packed slot s: key word tw[2 s], value word tw[2 s + 1] (little-endian u64)
+  uint32_t* const tw = reinterpret_cast<uint32_t*>(tile);
   auto step = [&](uint32_t k, uint32_t v, uint32_t lo, uint32_t ri, uint32_t& o) -> bool {
-    uint64_t w[STEP];
+    // key words only: a 4-byte gather per slot (the shared pipe is the kernel's limit)
+    uint32_t w[STEP];
 #pragma unroll
-    for (int u = 0; u < (int)STEP; ++u) w[u] = INS ? lds64(tile + lo + o + u) : tile[lo + o + u];
-    // first decisive slot, scanning backwards with selects (no mask building)
+    for (int q = 0; q < (int)STEP; ++q) w[q] = INS ? lds32(tw + 2 * (lo + o + q)) : tw[2 * (lo + o + q)];
+    // first decisive slot and its key word, scanning backwards with selects
     const uint32_t room = WINDOW - o;  // slots left in the window
-    uint32_t u = STEP;
+    uint32_t u = STEP, c = 0;
 #pragma unroll
     for (int q = (int)STEP - 1; q >= 0; --q) {
-      const uint32_t c = (uint32_t)w[q];
+      const uint32_t x = w[q];
       bool d;
-      if (INS) d = (c == k) | (adj ? (c - t) <= 1u : ((c == e) | (c == t)));
-      else d = (c == k) | (c == e);  // lookups pass tombstones
-      u = (d && (uint32_t)q < room) ? (uint32_t)q : u;
+      if (INS) d = (x == k) | (adj ? (x - t) <= 1u : ((x == e) | (x == t)));
+      else d = (x == k) | (x == e);  // lookups pass tombstones
+      d = d && (uint32_t)q < room;
+      u = d ? (uint32_t)q : u;
+      c = d ? x : c;
     }
     if (u == STEP) {
       o += STEP;
@@ -646,8 +651,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
       return false;
     }
     o += u;
-    const uint64_t wd = INS ? lds64(tile + lo + o) : tile[lo + o];
-    const uint32_t c = (uint32_t)wd;
+    const uint32_t s2 = 2 * (lo + o);
     if (INS) {
       if (c == k) {  // present before the first free cell (single_table.py:198-200)
         status[ri] = ST_DUPLICATE;
@@ -657,21 +661,19 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
         ndef += 1;
         return false;
       } else {
-        bool won = false;
-        if (c == e) {
-          const unsigned long long want = ((unsigned long long)v << 32) | k;
-          won = atomicCAS((unsigned long long*)(tile + lo + o), (unsigned long long)wd, want) == wd;
-        }
-        if (!won) {  // another key took it: re-read from this slot (single_table.py:232-233)
+        // claim the key word (32-bit CAS); the value word follows with a plain store:
+        // nothing in this pass reads values, and the write-back runs after a barrier
+        if (atomicCAS(tw + s2, e, k) != e) {  // another key took it: re-read from this slot (:232-233)
           att += ug;
           return true;
         }
+        tw[s2 + 1] = v;
         occ += 1;
         claimed_any = true;  // status: INSERTED is pre-set (staged_insert)
       }
     } else {
       const bool hit = c == k;
-      res_val[ri] = hit ? (uint32_t)(wd >> 32) : 0u;
+      res_val[ri] = hit ? tw[s2 + 1] : 0u;
       res_flag[ri] = (uint8_t)hit;
     }
     ops += 1;
