@@ -523,3 +523,26 @@ def test_staged_round2_and_fallback_caps_match_direct(tmp_path):
     env = dict(os.environ, CH_STAGED_ROUND2="1", CH_STAGED_FB_CTAS="1")
     r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("min_cap", [(1 << 31) - (1 << 20), (1 << 31) + (1 << 20)])
+def test_probe_start_matches_reference_hash_at_2g_slots(min_cap):
+    """Window starts h = mix64(k) mod c on both sides of c = 2^31 (the device takes a
+    32-bit remainder below 2^31, probing.py HashFn(0) % c): in a sparse table almost every
+    key sits at h, and every key sits inside window 0."""
+    from paper_2009_07914_b200.probing import mix64
+    t = SingleValueHashTable(min_cap, layout="packed", key_bits=32, value_bits=32, group_width=8)
+    c = t.capacity
+    assert (c < (1 << 31)) == (min_cap < (1 << 31))
+    rng = np.random.default_rng(11)
+    keys = np.unique(rng.integers(1, (1 << 32) - 2, size=200_000, dtype=np.uint64)).astype(np.uint32)
+    kt = torch.from_numpy(keys.view(np.int32)).cuda()
+    assert (t.insert_device(kt, kt).cpu() == 0).all()
+    slots, _, _, _ = t.find_device(kt)
+    slots = slots.cpu().numpy()
+    h = np.array([mix64(int(k)) % c for k in keys], dtype=np.int64)
+    off = (slots - h) % c
+    assert (off < 32).all()
+    assert (off == 0).mean() > 0.99
+    del t
+    torch.cuda.empty_cache()
