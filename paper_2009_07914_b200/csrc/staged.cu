@@ -32,6 +32,7 @@
 // (bucket, tile) runs, and records where each element went (u16 rank inside the
 // tile, per-tile run table), so results return by gathering the same runs --
 // every pass reads and writes coalesced and no position is carried per key.
+#include <algorithm>
 #include <cstdlib>
 
 #include "dispatch.cuh"
@@ -103,10 +104,13 @@ __device__ __forceinline__ void fence_smem_to_async() { asm volatile("fence.prox
 
 // ------------------------------------------------------------- count
 // Region histogram of the batch (dynamic shared memory, one counter per region).
+// gate: run only when *gate != 0 (the count-mode redo of an overflowed level-1 pass).
 __global__ void __launch_bounds__(1024) k_st_count(TableRef T, const uint32_t* __restrict__ keys, uint64_t n,
                                                    uint32_t regions, uint32_t* __restrict__ gcount,
-                                                   const unsigned long long* __restrict__ n_dev, int wj) {
+                                                   const unsigned long long* __restrict__ n_dev, int wj,
+                                                   const int* __restrict__ gate) {
   extern __shared__ uint32_t s_cnt[];
+  if (gate && *gate == 0) return;
   if (n_dev) n = *n_dev;
   for (uint32_t i = threadIdx.x; i < regions; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
@@ -146,25 +150,42 @@ __global__ void __launch_bounds__(1024) k_st_count(TableRef T, const uint32_t* _
     if (s_cnt[r]) atomicAdd(&gcount[r], s_cnt[r]);
 }
 
-// Cursors (region starts, super-region starts) and the L2 tile map: the L2 pass
-// cuts every super-region into its own 4096-element tiles, so a tile never
-// spans two super-regions (<= 256 buckets).  tstart[b] = first L2 tile of
-// super-region b, tstart[supers] = number of L2 tiles.  One CTA of PT threads.
-__global__ void __launch_bounds__(PT) k_st_plan(const uint64_t* __restrict__ foff, uint32_t regions,
-                                                uint32_t supers, uint32_t* __restrict__ cur1,
-                                                uint32_t* __restrict__ cur2, uint32_t* __restrict__ tstart) {
-  for (uint32_t i = threadIdx.x; i < regions; i += PT) cur2[i] = (uint32_t)foff[i];
+struct DeferOut {
+  uint32_t *k, *v, *x;
+  uint32_t* o;
+  unsigned long long* count;
+};
+
+// Partition state of one forward round.  Count mode: region offsets (foff) from the
+// count pass; cursors hold absolute positions.  Overallocated mode (the common big
+// batch, no count pass): super-region b owns [b cs, (b + 1) cs) of the level-1 order and
+// region r owns [r cr, (r + 1) cr) of the region order; cursors count from there.  A
+// level-1 run that does not fit raises `flag` and the count-mode level 1 is redone
+// (gated kernels, no host round trip); a level-2 run that does not fit is handed to
+// the COPS kernels through list A with result positions past regions * cr.
+struct Part {
+  const uint64_t* foff;      // count mode: region offsets (regions + 1); nullptr when overallocated
+  uint32_t* sbase;           // per super-region: first element of its level-1 area
+  uint32_t* scnt;            // per super-region: elements
+  uint32_t* tstart;          // per super-region: first level-2 tile; [supers] = level-2 tiles
+  uint32_t* cur1;            // level-1 run cursors
+  uint32_t* cur2;            // level-2 run cursors
+  uint32_t* lim2;            // overallocated: smallest start of an overflowing run per region
+  uint32_t cs, cr;           // overallocated capacities per super-region / region (0: count mode)
+  int* flag;                 // level-1 overflow
+  const int* gate;           // count-mode redo kernels run only when *gate != 0 (nullptr: always)
+  unsigned long long* ovf2;  // level-2 overflow results: positions ovf2_base + ...
+  uint32_t ovf2_base;
+  DeferOut da;               // level-2 overflow keys -> list A (resume at window 0)
+};
+
+// tstart from per-super-region element counts (one CTA of PT threads)
+__device__ __forceinline__ void plan_tiles(const uint32_t* scnt, uint32_t supers, uint32_t* tstart) {
   __shared__ uint32_t wt[PT / 32];
   uint32_t carry = 0;
   for (uint32_t b0 = 0; b0 < supers; b0 += PT) {
     const uint32_t b = b0 + threadIdx.x;
-    uint32_t v = 0;
-    if (b < supers) {
-      const uint64_t s = foff[(uint64_t)b << ST_S2];
-      const uint64_t e = foff[((uint64_t)(b + 1) << ST_S2) < regions ? ((uint64_t)(b + 1) << ST_S2) : regions];
-      cur1[b] = (uint32_t)s;
-      v = (uint32_t)((e - s + PTILE - 1) / PTILE);
-    }
+    const uint32_t v = b < supers ? (scnt[b] + PTILE - 1) / PTILE : 0u;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t x = v;
 #pragma unroll
@@ -186,6 +207,37 @@ __global__ void __launch_bounds__(PT) k_st_plan(const uint64_t* __restrict__ fof
   if (threadIdx.x == 0) tstart[supers] = carry;
 }
 
+// Count mode: cursors (super-region starts; region starts when level 2 is count mode
+// too) and the level-2 tile map: the L2 pass cuts every super-region into its own
+// 4096-element tiles, so a tile never spans two super-regions (<= 256 buckets).
+__global__ void __launch_bounds__(PT) k_st_plan(Part P, uint32_t regions, uint32_t supers, int init_cur2) {
+  if (P.gate && *P.gate == 0) return;
+  const uint64_t* foff = P.foff;
+  if (init_cur2)
+    for (uint32_t i = threadIdx.x; i < regions; i += PT) P.cur2[i] = (uint32_t)foff[i];
+  for (uint32_t b = threadIdx.x; b < supers; b += PT) {
+    const uint64_t s = foff[(uint64_t)b << ST_S2];
+    const uint64_t e = foff[((uint64_t)(b + 1) << ST_S2) < regions ? ((uint64_t)(b + 1) << ST_S2) : regions];
+    P.cur1[b] = (uint32_t)s;
+    P.sbase[b] = (uint32_t)s;
+    P.scnt[b] = (uint32_t)(e - s);
+  }
+  __syncthreads();
+  plan_tiles(P.scnt, supers, P.tstart);
+}
+
+// Overallocated level 1 done without overflow: super-region geometry from its cursors
+// (after an overflow the count-mode plan has set it already).
+__global__ void __launch_bounds__(PT) k_st_plan_oa(Part P, uint32_t supers) {
+  if (*P.flag) return;
+  for (uint32_t b = threadIdx.x; b < supers; b += PT) {
+    P.sbase[b] = b * P.cs;
+    P.scnt[b] = P.cur1[b];
+  }
+  __syncthreads();
+  plan_tiles(P.scnt, supers, P.tstart);
+}
+
 // Geometry of partition tile `t` of level L.  Level 1 tiles are the input cut in
 // PTILE pieces; level 2 tiles are each super-region (input: level-1 order) cut in
 // PTILE pieces.  Returns false for CTAs past the last tile.
@@ -198,8 +250,8 @@ struct TileGeo {
 };
 
 template <int L>
-__device__ __forceinline__ bool tile_geo(uint32_t t, uint64_t n, const uint64_t* __restrict__ foff,
-                                         const uint32_t* sup, uint32_t regions, TileGeo& g) {
+__device__ __forceinline__ bool tile_geo(uint32_t t, uint64_t n, const Part& P, const uint32_t* sup,
+                                         TileGeo& g) {
   if (L == 1) {
     g.pos0 = (uint64_t)t * PTILE;
     if (g.pos0 >= n) return false;
@@ -209,24 +261,24 @@ __device__ __forceinline__ bool tile_geo(uint32_t t, uint64_t n, const uint64_t*
   }
   const uint32_t lo = sup[0];  // the tile's super-region and its first tile (tile_super)
   if (lo == NO_SUPER) return false;
-  const uint64_t r0 = (uint64_t)lo << ST_S2;
-  const uint64_t r1 = ((uint64_t)(lo + 1) << ST_S2) < regions ? ((uint64_t)(lo + 1) << ST_S2) : regions;
-  const uint64_t s = foff[r0], e = foff[r1];
-  g.pos0 = s + (uint64_t)(t - sup[1]) * PTILE;
-  g.cnt = (uint32_t)((e - g.pos0) < PTILE ? (e - g.pos0) : PTILE);
-  g.cbase = (uint32_t)r0;
+  const uint32_t off = (t - sup[1]) * PTILE, cnt = sup[3];
+  g.pos0 = (uint64_t)sup[2] + off;
+  g.cnt = (cnt - off) < PTILE ? (cnt - off) : PTILE;
+  g.cbase = lo << ST_S2;
   return true;
 }
 
 // Level 2: the super-region owning tile t (tstart[b] <= t < tstart[b + 1]), found by
 // the CTA in one compare per thread (a per-thread binary search was 7% of the
 // split's instructions); sup[0] = the super-region or NO_SUPER, sup[1] = its first tile.
-__device__ __forceinline__ void tile_super(uint32_t t, const uint32_t* __restrict__ tstart, uint32_t supers,
-                                           uint32_t* sup) {
+__device__ __forceinline__ void tile_super(uint32_t t, const Part& P, uint32_t supers, uint32_t* sup) {
   // every load before the first branch: one L2 round trip (supers <= blockDim.x)
+  const uint32_t* tstart = P.tstart;
   const uint32_t tot = tstart[supers];
   const uint32_t i = threadIdx.x;
-  const uint32_t a = i < supers ? tstart[i] : 0u, b = i < supers ? tstart[i + 1] : 0u;
+  const bool own = i < supers;
+  const uint32_t a = own ? tstart[i] : 0u, b = own ? tstart[i + 1] : 0u;
+  const uint32_t sb = own ? P.sbase[i] : 0u, sc = own ? P.scnt[i] : 0u;
   if (t >= tot) {  // past the last tile (CTA-uniform)
     sup[0] = NO_SUPER;
     return;
@@ -234,6 +286,8 @@ __device__ __forceinline__ void tile_super(uint32_t t, const uint32_t* __restric
   if (a <= t && t < b) {
     sup[0] = i;
     sup[1] = a;
+    sup[2] = sb;
+    sup[3] = sc;
   }
   __syncthreads();
 }
@@ -279,9 +333,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define CH_AB_SPLIT_MINB 3  // 3 CTAs per SM (<= 42 registers, small spills): 26.5 -> 27.1 G ops/s
 #endif
 template <int L, int NPAY>
-__global__ void __launch_bounds__(PT, CH_AB_SPLIT_MINB) k_st_split(TableRef T, uint64_t n, const uint64_t* __restrict__ foff,
-                                                    const uint32_t* __restrict__ tstart, uint32_t supers,
-                                                    uint32_t regions, uint32_t ntiles,
+__global__ void __launch_bounds__(PT, CH_AB_SPLIT_MINB) k_st_split(TableRef T, uint64_t n, Part P, uint32_t supers,
+                                                    uint32_t ntiles,
                                                     const uint32_t* __restrict__ kin,
                                                     const uint32_t* __restrict__ vin,
                                                     const uint32_t* __restrict__ pin,
@@ -290,7 +343,6 @@ __global__ void __launch_bounds__(PT, CH_AB_SPLIT_MINB) k_st_split(TableRef T, u
                                                     uint32_t* __restrict__ rout,
                                                     uint16_t* __restrict__ lo_out, uint16_t* __restrict__ inv,
                                                     uint16_t* __restrict__ th, uint32_t* __restrict__ tg, uint32_t nb,
-                                                    uint32_t* __restrict__ cursor,
                                                     const unsigned long long* __restrict__ n_dev, int wj) {
   constexpr bool VALS = NPAY >= 1;
   constexpr bool POS = NPAY >= 2;
@@ -302,72 +354,100 @@ __global__ void __launch_bounds__(PT, CH_AB_SPLIT_MINB) k_st_split(TableRef T, u
   uint32_t* sR = sP + (POS ? PTILE : 0);
   uint16_t* sD = reinterpret_cast<uint16_t*>(sR + (RES ? PTILE : 0));
   uint16_t* sL = sD + PTILE;  // level 2 only
+  if (P.gate && *P.gate == 0) return;
   if (n_dev) n = *n_dev;
-  __shared__ uint32_t hist[PBINS], boff[PBINS], gbase[PBINS];
+  __shared__ uint32_t hist[PBINS], boff[PBINS], gbase[PBINS], dbase[PBINS];
+  __shared__ uint8_t smode[PBINS];  // 0: run written, 1: dropped (level-1 overflow), 2: to list A
   __shared__ uint32_t wt[PT / 32];
-  const uint32_t t = blockIdx.x;
-  __shared__ uint32_t s_sup[2];
-  if (L == 2) {
-    if (t >= ntiles) return;
-    tile_super(t, tstart, supers, s_sup);
-  }
-  TileGeo g;
-  if (t >= ntiles || !tile_geo<L>(t, n, foff, s_sup, regions, g)) return;
-  hist[threadIdx.x] = 0;  // PBINS == PT
-  uint32_t k[PI], v[PI], q[PI], w[PI], d[PI], r[PI];
+  __shared__ uint32_t s_sup[4];
+  const uint32_t cap = L == 1 ? P.cs : P.cr;
+  uint32_t* const cursor = L == 1 ? P.cur1 : P.cur2;
+  // persistent CTAs (a gated redo exits in one wave)
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (L == 2) tile_super(t, P, supers, s_sup);
+    TileGeo g;
+    if (!tile_geo<L>(t, n, P, s_sup, g)) break;  // tiles past the end are past it for every later t
+    hist[threadIdx.x] = 0;  // PBINS == PT
+    uint32_t k[PI], v[PI], q[PI], w[PI], d[PI], r[PI];
 #pragma unroll
-  for (int it = 0; it < PI; ++it) {  // all loads in flight before any use
-    const uint32_t li = (uint32_t)it * PT + threadIdx.x;
-    k[it] = li < g.cnt ? __ldcs(kin + g.pos0 + li) : 0u;
-    if (VALS) v[it] = li < g.cnt ? __ldcs(vin + g.pos0 + li) : 0u;
-    if (POS) q[it] = li < g.cnt ? __ldcs(pin + g.pos0 + li) : 0u;
-    if (RES) w[it] = li < g.cnt ? __ldcs(rin + g.pos0 + li) : 0u;
-  }
-  __syncthreads();  // hist zeroed
+    for (int it = 0; it < PI; ++it) {  // all loads in flight before any use
+      const uint32_t li = (uint32_t)it * PT + threadIdx.x;
+      k[it] = li < g.cnt ? __ldcs(kin + g.pos0 + li) : 0u;
+      if (VALS) v[it] = li < g.cnt ? __ldcs(vin + g.pos0 + li) : 0u;
+      if (POS) q[it] = li < g.cnt ? __ldcs(pin + g.pos0 + li) : 0u;
+      if (RES) w[it] = li < g.cnt ? __ldcs(rin + g.pos0 + li) : 0u;
+    }
+    __syncthreads();  // hist zeroed
 #pragma unroll
-  for (int it = 0; it < PI; ++it) {
-    const uint32_t li = (uint32_t)it * PT + threadIdx.x;
-    if (li >= g.cnt) continue;
-    const uint32_t h = window_start(T, k[it], wj);
-    const uint32_t b = L == 1 ? (h >> ST_LOG_R) >> ST_S2 : (h >> ST_LOG_R) - g.cbase;
-    r[it] = atomicAdd(&hist[b], 1u);
-    d[it] = b | (L == 2 ? (h & (ST_R - 1)) << 16 : 0u);  // window start rides along (registers)
-  }
-  __syncthreads();
-  const uint32_t hv = hist[threadIdx.x];
-  // the run's global position: the atomic's round trip overlaps the bucketing below
-  const uint32_t gb = hv ? atomicAdd(&cursor[g.cbase + threadIdx.x], hv) : 0u;
-  const uint32_t bo = block_excl_scan(hv, wt);
-  boff[threadIdx.x] = bo;
-  __syncthreads();
+    for (int it = 0; it < PI; ++it) {
+      const uint32_t li = (uint32_t)it * PT + threadIdx.x;
+      if (li >= g.cnt) continue;
+      const uint32_t h = window_start(T, k[it], wj);
+      const uint32_t b = L == 1 ? (h >> ST_LOG_R) >> ST_S2 : (h >> ST_LOG_R) - g.cbase;
+      r[it] = atomicAdd(&hist[b], 1u);
+      d[it] = b | (L == 2 ? (h & (ST_R - 1)) << 16 : 0u);  // window start rides along (registers)
+    }
+    __syncthreads();
+    const uint32_t hv = hist[threadIdx.x];
+    const uint32_t bg = g.cbase + threadIdx.x;  // the bucket's cursor (super-region / region)
+    // the run's global position: the atomic's round trip overlaps the bucketing below
+    uint32_t old = hv ? atomicAdd(&cursor[bg], hv) : 0u;
+    const uint32_t bo = block_excl_scan(hv, wt);
+    boff[threadIdx.x] = bo;
+    __syncthreads();
 #pragma unroll
-  for (int it = 0; it < PI; ++it) {
-    const uint32_t li = (uint32_t)it * PT + threadIdx.x;
-    if (li >= g.cnt) continue;
-    const uint32_t b = d[it] & 0xFFFFu;
-    const uint32_t j = boff[b] + r[it];
-    sK[j] = k[it];
-    if (VALS) sV[j] = v[it];
-    if (POS) sP[j] = q[it];
-    if (RES) sR[j] = w[it];
-    sD[j] = (uint16_t)b;
-    if (L == 2) sL[j] = (uint16_t)(d[it] >> 16);
-    if (inv) inv[g.pos0 + li] = (uint16_t)j;
-  }
-  gbase[threadIdx.x] = gb - bo;  // run destination minus its tile offset (u32 wrap is fine)
-  if (th && threadIdx.x < nb) {
-    th[(uint64_t)t * nb + threadIdx.x] = (uint16_t)hv;
-    tg[(uint64_t)t * nb + threadIdx.x] = gb;
-  }
-  __syncthreads();
-  for (uint32_t j = threadIdx.x; j < g.cnt; j += PT) {
-    const uint32_t b = sD[j];
-    const uint32_t dst = gbase[b] + j;
-    kout[dst] = sK[j];
-    if (VALS) vout[dst] = sV[j];
-    if (POS) pout[dst] = sP[j];
-    if (RES) rout[dst] = sR[j];
-    if (L == 2) lo_out[dst] = sL[j];
+    for (int it = 0; it < PI; ++it) {
+      const uint32_t li = (uint32_t)it * PT + threadIdx.x;
+      if (li >= g.cnt) continue;
+      const uint32_t b = d[it] & 0xFFFFu;
+      const uint32_t j = boff[b] + r[it];
+      sK[j] = k[it];
+      if (VALS) sV[j] = v[it];
+      if (POS) sP[j] = q[it];
+      if (RES) sR[j] = w[it];
+      sD[j] = (uint16_t)b;
+      if (L == 2) sL[j] = (uint16_t)(d[it] >> 16);
+      if (inv) inv[g.pos0 + li] = (uint16_t)j;
+    }
+    uint8_t mode = 0;
+    uint32_t gb = (cap ? bg * cap : 0u) + old;
+    if (cap && hv && old + hv > cap) {  // the bucket's area is full (skewed batch)
+      if (L == 1) {
+        *P.flag = 1;  // the count-mode level 1 runs again
+        mode = 1;
+      } else {
+        atomicMin(&P.lim2[bg], old);  // the region's keys end before this run
+        gb = P.ovf2_base + (uint32_t)atomicAdd(P.ovf2, (unsigned long long)hv);
+        dbase[threadIdx.x] = (uint32_t)atomicAdd(P.da.count, (unsigned long long)hv) - bo;
+        mode = 2;
+      }
+    }
+    smode[threadIdx.x] = mode;
+    gbase[threadIdx.x] = gb - bo;  // run destination minus its tile offset (u32 wrap is fine)
+    if (th && threadIdx.x < nb) {
+      th[(uint64_t)t * nb + threadIdx.x] = (uint16_t)hv;
+      tg[(uint64_t)t * nb + threadIdx.x] = gb;
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < g.cnt; j += PT) {
+      const uint32_t b = sD[j];
+      const uint32_t dst = gbase[b] + j;
+      const uint8_t md = smode[b];
+      if (md == 0) {
+        kout[dst] = sK[j];
+        if (VALS) vout[dst] = sV[j];
+        if (POS) pout[dst] = sP[j];
+        if (RES) rout[dst] = sR[j];
+        if (L == 2) lo_out[dst] = sL[j];
+      } else if (L == 2 && md == 2) {  // COPS kernels from window 0; result at dst
+        const uint32_t a = dbase[b] + j;
+        P.da.k[a] = sK[j];
+        if (VALS) P.da.v[a] = sV[j];
+        P.da.x[a] = dst;
+        P.da.o[a] = 0;
+      }
+    }
+    __syncthreads();  // shared buffers are reused by the next tile
   }
 }
 
@@ -381,9 +461,7 @@ __global__ void __launch_bounds__(PT, CH_AB_SPLIT_MINB) k_st_split(TableRef T, u
 #define CH_AB_GATHER_MINB 3  // 3 CTAs per SM (<= 42 registers): 57-58 registers ran 2 and measured slower
 #endif
 template <int L, bool VAL>
-__global__ void __launch_bounds__(PT, CH_AB_GATHER_MINB) k_st_gather(uint64_t n, const uint64_t* __restrict__ foff,
-                                                  const uint32_t* __restrict__ tstart, uint32_t supers,
-                                                  uint32_t regions, uint32_t ntiles,
+__global__ void __launch_bounds__(PT, CH_AB_GATHER_MINB) k_st_gather(uint64_t n, Part P, uint32_t supers, uint32_t ntiles,
                                                   const uint16_t* __restrict__ inv,
                                                   const uint16_t* __restrict__ th, const uint32_t* __restrict__ tg,
                                                   uint32_t nb, const uint32_t* __restrict__ src_v,
@@ -396,7 +474,7 @@ __global__ void __launch_bounds__(PT, CH_AB_GATHER_MINB) k_st_gather(uint64_t n,
   __shared__ uint32_t gsrc[PBINS];
   __shared__ uint32_t wt[PT / 32];
   const uint32_t t = blockIdx.x;
-  __shared__ uint32_t s_sup[2];
+  __shared__ uint32_t s_sup[4];
   if (t >= ntiles) return;
   // every status INSERTED (insert without exceptions): nothing to move back
   const bool skip = !VAL && exc && *exc == 0;
@@ -406,32 +484,10 @@ __global__ void __launch_bounds__(PT, CH_AB_GATHER_MINB) k_st_gather(uint64_t n,
   const uint32_t gs = rt ? tg[(uint64_t)t * nb + threadIdx.x] : 0u;
   if (L == 2) {
     if (skip) return;  // level 1 writes the statuses
-#ifdef CH_AB_GATHER_BSEARCH
-    __shared__ uint32_t s_ts[PBINS + 1];
-    for (uint32_t i = threadIdx.x; i <= supers; i += PT) s_ts[i] = tstart[i];
-    __syncthreads();
-    if (t >= s_ts[supers]) {
-      s_sup[0] = NO_SUPER;
-    } else {
-      uint32_t lo = 0, hi = supers;
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s_ts[mid] <= t) lo = mid;
-        else hi = mid;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        s_sup[0] = lo;
-        s_sup[1] = s_ts[lo];
-      }
-    }
-    __syncthreads();
-#else
-    tile_super(t, tstart, supers, s_sup);
-#endif
+    tile_super(t, P, supers, s_sup);
   }
   TileGeo g;
-  if (t >= ntiles || !tile_geo<L>(t, n, foff, s_sup, regions, g)) return;
+  if (t >= ntiles || !tile_geo<L>(t, n, P, s_sup, g)) return;
   if (skip) {
     if (L == 1)
       for (uint32_t li = threadIdx.x; li < g.cnt; li += PT) dst_f[g.pos0 + li] = ST_INSERTED;
@@ -501,11 +557,6 @@ struct DeferBuf {
   unsigned long long gb;
 };
 
-struct DeferOut {
-  uint32_t *k, *v, *x;
-  uint32_t* o;
-  unsigned long long* count;
-};
 
 template <bool VALS, uint32_t CAP>
 __device__ __forceinline__ void defer_push(DeferBuf<VALS, CAP>& B, const DeferOut& D, uint32_t k, uint32_t v,
@@ -574,7 +625,7 @@ constexpr uint32_t DBUF_B = 1024;  // window-full deferrals buffered per region 
 constexpr uint32_t NONE = 0xffffffffu;
 
 template <int MODE, bool R2>
-__global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* __restrict__ foff,
+__global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
                                                     const uint32_t* __restrict__ keys,
                                                     const uint32_t* __restrict__ vals,
                                                     const uint32_t* __restrict__ pos,
@@ -593,9 +644,17 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, const uint64_t* 
   __shared__ __align__(8) uint64_t bar;
   __shared__ int dirty;
   const uint32_t f = blockIdx.x;
-  const uint64_t k0 = foff[f], k1 = foff[f + 1];
-  if (k0 == k1) return;  // no key starts in this region
-  const uint32_t m = (uint32_t)(k1 - k0);
+  uint64_t k0;
+  uint32_t m;
+  if (P.foff) {  // count mode
+    k0 = P.foff[f];
+    m = (uint32_t)(P.foff[f + 1] - k0);
+  } else {  // overallocated: the region's area, up to its first overflowing run
+    k0 = (uint64_t)f * P.cr;
+    const uint32_t c2 = P.cur2[f], l2 = P.lim2[f];
+    m = c2 < l2 ? c2 : l2;
+  }
+  if (m == 0) return;  // no key starts in this region
   const uint64_t rbase = (uint64_t)f << ST_LOG_R;
   const uint32_t len = (uint32_t)((T.c - rbase) < ST_R ? (T.c - rbase) : ST_R);
   uint64_t* slots = static_cast<uint64_t*>(T.slots);
@@ -777,14 +836,28 @@ constexpr size_t probe_smem() {
 struct StPlan {
   uint32_t regions, supers;
   uint64_t tiles1, tiles2;  // partition tiles per level (level 2: upper bound)
+  bool oa;                  // round 1 overallocated (no count pass)
+  uint32_t cs, cr;          // its capacities per super-region / region
+  uint64_t n1, n2, nres;    // level-1 / level-2 array lengths, region-order results (+ overflow)
 };
 
+// Overallocation: expected keys per region n R / c plus 6.25 % and 256 (> 8 standard
+// deviations of a uniform hash at the bench's 7.8 K keys per region), per super-region
+// + 3 % and one tile (> 40 deviations).  Skewed batches overflow and take the exact
+// paths (Part).  Positions stay below 2^32 for n < 2^30.
 static StPlan st_plan(const TableRef& T, uint64_t n) {
   StPlan p;
   p.regions = (uint32_t)((T.c + ST_R - 1) >> ST_LOG_R);
   p.supers = (p.regions + (1u << ST_S2) - 1) >> ST_S2;
   p.tiles1 = (n + PTILE - 1) / PTILE;
   p.tiles2 = p.tiles1 + p.supers;
+  p.oa = n < (1ull << 30);
+  const double per_region = (double)n * ST_R / (double)T.c;
+  p.cs = p.oa ? (uint32_t)(per_region * (1u << ST_S2) * 1.03) + PTILE : 0u;
+  p.cr = p.oa ? (uint32_t)(per_region * 1.0625) + 256u : 0u;
+  p.n1 = p.oa ? std::max<uint64_t>(n, (uint64_t)p.supers * p.cs) : n;
+  p.n2 = p.oa ? (uint64_t)p.regions * p.cr : n;
+  p.nres = p.oa ? p.n2 + n : n;
   return p;
 }
 
@@ -808,7 +881,10 @@ struct Carver {
 
 // One forward round: histogram + scan + plan + one or two tile partitions.
 struct Round {
-  uint32_t *gcount, *cur1, *cur2, *tstart;
+  uint32_t *gcount, *cur1, *cur2, *tstart, *sbase, *scnt, *lim2;
+  int* flag;
+  unsigned long long* ovf2;
+  Part part;  // the geometry the round's kernels ran with (probe, gathers)
   uint64_t* foff;
   void* scan;
   size_t scan_bytes;
@@ -826,29 +902,36 @@ struct StBufs {
   uint8_t *rf, *rf1;   // lookup: found flags; insert: statuses
 };
 
-static void carve_round(Carver& c, Round& r, const StPlan& p, uint64_t n, int npay, bool inverse, int levels) {
+static void carve_round(Carver& c, Round& r, const StPlan& p, uint64_t n, int npay, bool inverse, int levels,
+                        bool oa) {
   r = Round{};
+  const uint64_t n1 = oa ? p.n1 : n, n2 = oa ? p.n2 : n;
   r.gcount = (uint32_t*)c.take(p.regions * 4ull);
+  r.sbase = (uint32_t*)c.take(p.supers * 4ull);
+  r.scnt = (uint32_t*)c.take(p.supers * 4ull);
+  r.lim2 = (uint32_t*)c.take(p.regions * 4ull);
+  r.ovf2 = (unsigned long long*)c.take(64);
+  r.flag = reinterpret_cast<int*>(r.ovf2 + 1);
   r.foff = (uint64_t*)c.take((p.regions + 1ull) * 8);
   r.scan_bytes = align_up(exclusive_scan_scratch_bytes(p.regions));
   r.scan = c.take(r.scan_bytes);
   r.cur1 = (uint32_t*)c.take(PBINS * 4ull);
   r.cur2 = (uint32_t*)c.take(p.regions * 4ull);
   r.tstart = (uint32_t*)c.take((p.supers + 1ull) * 4);
-  r.k1 = (uint32_t*)c.take(n * 4);
-  r.v1 = npay >= 1 ? (uint32_t*)c.take(n * 4) : nullptr;
-  r.p1 = npay >= 2 ? (uint32_t*)c.take(n * 4) : nullptr;
-  r.r1 = npay >= 3 ? (uint32_t*)c.take(n * 4) : nullptr;
+  r.k1 = (uint32_t*)c.take(n1 * 4);
+  r.v1 = npay >= 1 ? (uint32_t*)c.take(n1 * 4) : nullptr;
+  r.p1 = npay >= 2 ? (uint32_t*)c.take(n1 * 4) : nullptr;
+  r.r1 = npay >= 3 ? (uint32_t*)c.take(n1 * 4) : nullptr;
   if (levels == 2) {
-    r.k2 = (uint32_t*)c.take(n * 4);
-    r.v2 = npay >= 1 ? (uint32_t*)c.take(n * 4) : nullptr;
-    r.p2 = npay >= 2 ? (uint32_t*)c.take(n * 4) : nullptr;
-    r.r2 = npay >= 3 ? (uint32_t*)c.take(n * 4) : nullptr;
-    r.lo2 = (uint16_t*)c.take(n * 2);
+    r.k2 = (uint32_t*)c.take(n2 * 4);
+    r.v2 = npay >= 1 ? (uint32_t*)c.take(n2 * 4) : nullptr;
+    r.p2 = npay >= 2 ? (uint32_t*)c.take(n2 * 4) : nullptr;
+    r.r2 = npay >= 3 ? (uint32_t*)c.take(n2 * 4) : nullptr;
+    r.lo2 = (uint16_t*)c.take(n2 * 2);
   }
   if (inverse) {
     r.inv1 = (uint16_t*)c.take(n * 2);
-    r.inv2 = (uint16_t*)c.take(n * 2);
+    r.inv2 = (uint16_t*)c.take(n1 * 2);
     r.th1 = (uint16_t*)c.take(p.tiles1 * p.supers * 2);
     r.tg1 = (uint32_t*)c.take(p.tiles1 * p.supers * 4);
     r.th2 = (uint16_t*)c.take(p.tiles2 * 256 * 2);
@@ -859,9 +942,9 @@ static void carve_round(Carver& c, Round& r, const StPlan& p, uint64_t n, int np
 static StBufs st_carve(const StPlan& p, uint64_t n, bool ins, bool round2, void* base, size_t* total) {
   Carver c{static_cast<char*>(base)};
   StBufs b;
-  carve_round(c, b.r1, p, n, ins ? 1 : 0, true, 2);
-  if (round2) carve_round(c, b.r2, p, n, ins ? 2 : 1, false, 2);
-  carve_round(c, b.rd, p, n, ins ? 3 : 2, false, 1);
+  carve_round(c, b.r1, p, n, ins ? 1 : 0, true, 2, p.oa);
+  if (round2) carve_round(c, b.r2, p, n, ins ? 2 : 1, false, 2, false);
+  carve_round(c, b.rd, p, n, ins ? 3 : 2, false, 1, false);
   b.dcount = (unsigned long long*)c.take(64);
   b.ak = (uint32_t*)c.take(n * 4);
   b.av = ins ? (uint32_t*)c.take(n * 4) : nullptr;
@@ -871,10 +954,10 @@ static StBufs st_carve(const StPlan& p, uint64_t n, bool ins, bool round2, void*
   b.bv = round2 ? (ins ? (uint32_t*)c.take(n * 4) : nullptr) : b.av;
   b.bx = round2 ? (uint32_t*)c.take(n * 4) : b.ax;
   b.bo = round2 ? (uint32_t*)c.take(n * 4) : b.ao;
-  b.rv = ins ? nullptr : (uint32_t*)c.take(n * 4);
-  b.rv1 = ins ? nullptr : (uint32_t*)c.take(n * 4);
-  b.rf = (uint8_t*)c.take(n);
-  b.rf1 = (uint8_t*)c.take(n);
+  b.rv = ins ? nullptr : (uint32_t*)c.take(p.nres * 4);
+  b.rv1 = ins ? nullptr : (uint32_t*)c.take(p.n1 * 4);
+  b.rf = (uint8_t*)c.take(p.nres);
+  b.rf1 = (uint8_t*)c.take(p.n1);
   *total = c.used;
   return b;
 }
@@ -923,40 +1006,98 @@ static void st_timed_end(const Launch& lc, cudaEvent_t e0) {
   }
 }
 
-// One forward round over keys k (+ payloads v, q, w): count + scan + plan + L1 (+ L2).
-// n_dev: the round's count lives on the device (n is the capacity).  wj: window.
+// One forward round over keys k (+ payloads v, q, w).  Count mode: count + scan + plan +
+// L1 (+ L2).  Overallocated (round 1 with p.oa, da = list A): L1 into fixed areas; the
+// count-mode L1 runs again only if a run overflowed (gated kernels); L2 into fixed
+// region areas, overflowing runs to list A.  n_dev: the round's count lives on the
+// device (n is the capacity).  wj: window.
 template <int NPAY>
-static int st_forward(const Launch& lc, const TableRef& T, const StPlan& p, const Round& r, const uint32_t* k,
+static int st_forward(const Launch& lc, const TableRef& T, const StPlan& p, Round& r, const uint32_t* k,
                       const uint32_t* v, const uint32_t* q, const uint32_t* w, uint64_t n,
-                      const unsigned long long* n_dev, int wj, int levels) {
-  int rc = cuda_check(cudaMemsetAsync(r.gcount, 0, p.regions * 4ull, lc.stream), "memset");
-  if (rc) return rc;
-  const size_t csmem = p.regions * 4ull;
-  if ((rc = st_smem(k_st_count, csmem))) return rc;
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_st_count, 1024, csmem);
-  if (occ < 1) occ = 1;
-  k_st_count<<<(unsigned)(lc.sms * occ), 1024, csmem, lc.stream>>>(T, k, n, p.regions, r.gcount, n_dev, wj);
-  count_launch();
-  if ((rc = cuda_check(cudaGetLastError(), "staged count"))) return rc;
-  if ((rc = exclusive_scan_u32(lc, r.gcount, p.regions, r.foff, r.scan, r.scan_bytes))) return rc;
-  k_st_plan<<<1, PT, 0, lc.stream>>>(r.foff, p.regions, p.supers, r.cur1, r.cur2, r.tstart);
-  count_launch();
-  // bucketed (k, payloads, bucket id, level 2: window start)
+                      const unsigned long long* n_dev, int wj, int levels, const DeferOut* da = nullptr) {
+  const bool oa = da != nullptr && p.oa && levels == 2 && n_dev == nullptr;
+  Part P{};
+  P.sbase = r.sbase;
+  P.scnt = r.scnt;
+  P.tstart = r.tstart;
+  P.cur1 = r.cur1;
+  P.cur2 = r.cur2;
+  P.lim2 = r.lim2;
+  P.flag = r.flag;
+  P.ovf2 = r.ovf2;
   const size_t sm1 = (size_t)PTILE * (4 + 4 * NPAY + 2), sm2 = sm1 + PTILE * 2;
   const unsigned t1 = (unsigned)p.tiles1, t2 = (unsigned)p.tiles2;
   auto k1f = k_st_split<1, NPAY>;
-  if ((rc = st_smem(k1f, sm1))) return rc;
-  k1f<<<t1, PT, sm1, lc.stream>>>(T, n, r.foff, r.tstart, p.supers, p.regions, t1, k, v, q, w, r.k1, r.v1, r.p1, r.r1,
-                                   nullptr, r.inv1, r.th1, r.tg1, p.supers, r.cur1, n_dev, wj);
-  count_launch();
+  auto k2f = k_st_split<2, NPAY>;
+  int rc = st_smem(k1f, sm1);
+  if (!rc && levels == 2) rc = st_smem(k2f, sm2);
+  if (rc) return rc;
+  // persistent partition CTAs (a gated level 1 costs one wave)
+  auto grid = [&](const void* kern, size_t sm, unsigned tiles) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT, sm);
+    const unsigned full = (unsigned)lc.sms * (unsigned)(occ > 0 ? occ : 1);
+    return tiles < full ? (tiles ? tiles : 1u) : full;
+  };
+  // a CTA per tile when the batch size is known on the host (a persistent loop measured
+  // 26.8 vs 27.9 G ops/s); one persistent wave when it lives on the device (most of the
+  // grid would exit at once) and for the gated redo
+  const unsigned g1r = grid((const void*)k1f, sm1, t1);
+  const unsigned g1 = n_dev ? g1r : (t1 ? t1 : 1u);
+  const unsigned g2 = n_dev ? grid((const void*)k2f, sm2, t2) : (t2 ? t2 : 1u);
+  const size_t csmem = p.regions * 4ull;
+  if ((rc = st_smem(k_st_count, csmem))) return rc;
+  int cocc = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cocc, k_st_count, 1024, csmem);
+  if (cocc < 1) cocc = 1;
+  // count mode level 1 (always, or as the gated redo after an overflow)
+  auto count_mode_l1 = [&](Part C, int init_cur2) -> int {
+    int e = cuda_check(cudaMemsetAsync(r.gcount, 0, p.regions * 4ull, lc.stream), "memset");
+    if (e) return e;
+    k_st_count<<<(unsigned)(lc.sms * cocc), 1024, csmem, lc.stream>>>(T, k, n, p.regions, r.gcount, n_dev, wj,
+                                                                       C.gate);
+    count_launch();
+    if ((e = cuda_check(cudaGetLastError(), "staged count"))) return e;
+    if ((e = exclusive_scan_u32(lc, r.gcount, p.regions, r.foff, r.scan, r.scan_bytes))) return e;
+    k_st_plan<<<1, PT, 0, lc.stream>>>(C, p.regions, p.supers, init_cur2);
+    count_launch();
+    k1f<<<C.gate ? g1r : g1, PT, sm1, lc.stream>>>(T, n, C, p.supers, t1, k, v, q, w, r.k1, r.v1, r.p1, r.r1, nullptr,
+                                                    r.inv1, r.th1, r.tg1, p.supers, n_dev, wj);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "staged partition");
+  };
+  if (oa) {
+    P.cs = p.cs;
+    P.cr = p.cr;
+    P.ovf2_base = p.regions * p.cr;
+    P.da = *da;
+    rc = cuda_check(cudaMemsetAsync(r.cur1, 0, p.supers * 4ull, lc.stream), "memset");
+    if (!rc) rc = cuda_check(cudaMemsetAsync(r.cur2, 0, p.regions * 4ull, lc.stream), "memset");
+    if (!rc) rc = cuda_check(cudaMemsetAsync(r.lim2, 0xFF, p.regions * 4ull, lc.stream), "memset");
+    if (!rc) rc = cuda_check(cudaMemsetAsync(r.ovf2, 0, 64, lc.stream), "memset");  // ovf2, flag
+    if (rc) return rc;
+    Part L1 = P;
+    L1.cr = 0;
+    k1f<<<g1, PT, sm1, lc.stream>>>(T, n, L1, p.supers, t1, k, v, q, w, r.k1, r.v1, r.p1, r.r1, nullptr, r.inv1,
+                                     r.th1, r.tg1, p.supers, n_dev, wj);
+    count_launch();
+    Part C = P;  // the redo: count-mode cursors, level 2 stays overallocated
+    C.foff = r.foff;
+    C.cs = C.cr = 0;
+    C.gate = r.flag;
+    if ((rc = count_mode_l1(C, 0))) return rc;
+    k_st_plan_oa<<<1, PT, 0, lc.stream>>>(P, p.supers);
+    count_launch();
+  } else {
+    P.foff = r.foff;
+    if ((rc = count_mode_l1(P, levels == 2))) return rc;
+  }
   if (levels == 2) {
-    auto k2f = k_st_split<2, NPAY>;
-    if ((rc = st_smem(k2f, sm2))) return rc;
-    k2f<<<t2, PT, sm2, lc.stream>>>(T, n, r.foff, r.tstart, p.supers, p.regions, t2, r.k1, r.v1, r.p1, r.r1, r.k2,
-                                     r.v2, r.p2, r.r2, r.lo2, r.inv2, r.th2, r.tg2, 256, r.cur2, n_dev, wj);
+    k2f<<<g2, PT, sm2, lc.stream>>>(T, n, P, p.supers, t2, r.k1, r.v1, r.p1, r.r1, r.k2, r.v2, r.p2, r.r2, r.lo2,
+                                     r.inv2, r.th2, r.tg2, 256, n_dev, wj);
     count_launch();
   }
+  r.part = P;
   return cuda_check(cudaGetLastError(), "staged partition");
 }
 
@@ -968,11 +1109,10 @@ static int st_backward(const Launch& lc, const StPlan& p, const StBufs& b, uint6
   const unsigned t1 = (unsigned)p.tiles1, t2 = (unsigned)p.tiles2;
   auto g2 = k_st_gather<2, VAL>;
   auto g1 = k_st_gather<1, VAL>;
-  g2<<<t2, PT, 0, lc.stream>>>(n, r.foff, r.tstart, p.supers, p.regions, t2, r.inv2, r.th2, r.tg2, 256, rv, rf, b.rv1,
-                                b.rf1, exc);
+  g2<<<t2, PT, 0, lc.stream>>>(n, r.part, p.supers, t2, r.inv2, r.th2, r.tg2, 256, rv, rf, b.rv1, b.rf1, exc);
   count_launch();
-  g1<<<t1, PT, 0, lc.stream>>>(n, r.foff, r.tstart, p.supers, p.regions, t1, r.inv1, r.th1, r.tg1, p.supers, b.rv1,
-                                b.rf1, out_v, out_f, exc);
+  g1<<<t1, PT, 0, lc.stream>>>(n, r.part, p.supers, t1, r.inv1, r.th1, r.tg1, p.supers, b.rv1, b.rf1, out_v, out_f,
+                                exc);
   count_launch();
   return cuda_check(cudaGetLastError(), "staged gather");
 }
@@ -987,8 +1127,8 @@ static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const 
   if (rc) return rc;
   cudaEvent_t e0;
   if (!R2) st_timed(lc, &e0);  // the dominant kernel of the staged schedule (bench.py roofline)
-  kern<<<p.regions, RT, sm, lc.stream>>>(T, r.foff, r.k2, MODE == 0 ? r.v2 : nullptr, pos, r.lo2, status, rv, rf, DA,
-                                         DB, g, exc);
+  kern<<<p.regions, RT, sm, lc.stream>>>(T, r.part, r.k2, MODE == 0 ? r.v2 : nullptr, pos, r.lo2, status, rv, rf,
+                                         DA, DB, g, exc);
   count_launch();
   if (!R2) st_timed_end(lc, e0);
   return cuda_check(cudaGetLastError(), "staged region probe");
@@ -999,16 +1139,16 @@ int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
   const StPlan p = st_plan(T, n);
   size_t total = 0;
   const bool r2 = g_round2;
-  const StBufs b = st_carve(p, n, true, r2, scratch, &total);
+  StBufs b = st_carve(p, n, true, r2, scratch, &total);
   int rc = cuda_check(cudaMemsetAsync(b.dcount, 0, 24, lc.stream), "memset");  // lists A, B; exceptions
-  if (!rc) rc = cuda_check(cudaMemsetAsync(b.rf, ST_INSERTED, n, lc.stream), "memset");  // exceptions overwrite
+  if (!rc) rc = cuda_check(cudaMemsetAsync(b.rf, ST_INSERTED, p.nres, lc.stream), "memset");  // exceptions overwrite
   unsigned long long* exc = b.dcount + 2;
-  if (!rc)
-    rc = st_forward<1>(lc, T, p, b.r1, (const uint32_t*)keys, (const uint32_t*)vals, nullptr, nullptr, n, nullptr, 0,
-                       2);
-  if (rc) return rc;
   const DeferOut DA{b.ak, b.av, b.ax, b.ao, b.dcount};
   const DeferOut DB{b.bk, b.bv, b.bx, b.bo, r2 ? b.dcount + 1 : b.dcount};
+  if (!rc)
+    rc = st_forward<1>(lc, T, p, b.r1, (const uint32_t*)keys, (const uint32_t*)vals, nullptr, nullptr, n, nullptr, 0,
+                       2, &DA);
+  if (rc) return rc;
   if ((rc = st_probe<0, false>(lc, T, p, b.r1, nullptr, b.rf, nullptr, nullptr, DA, DB, ts.g, exc))) return rc;
   if (r2) {  // window 1 of the keys whose window 0 was full, staged the same way
     if ((rc = st_forward<2>(lc, T, p, b.r2, b.bk, b.bv, b.bx, nullptr, n, b.dcount + 1, 1, 2))) return rc;
@@ -1034,12 +1174,13 @@ int staged_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
   const StPlan p = st_plan(T, n);
   size_t total = 0;
   const bool r2 = g_round2;
-  const StBufs b = st_carve(p, n, false, r2, scratch, &total);
+  StBufs b = st_carve(p, n, false, r2, scratch, &total);
   int rc = cuda_check(cudaMemsetAsync(b.dcount, 0, 16, lc.stream), "memset");
-  if (!rc) rc = st_forward<0>(lc, T, p, b.r1, (const uint32_t*)keys, nullptr, nullptr, nullptr, n, nullptr, 0, 2);
-  if (rc) return rc;
   const DeferOut DA{b.ak, nullptr, b.ax, b.ao, b.dcount};
   const DeferOut DB{b.bk, nullptr, b.bx, b.bo, r2 ? b.dcount + 1 : b.dcount};
+  if (!rc)
+    rc = st_forward<0>(lc, T, p, b.r1, (const uint32_t*)keys, nullptr, nullptr, nullptr, n, nullptr, 0, 2, &DA);
+  if (rc) return rc;
   if ((rc = st_probe<1, false>(lc, T, p, b.r1, nullptr, nullptr, b.rv, b.rf, DA, DB, ts.g))) return rc;
   if (r2) {  // window 1 of the keys whose window 0 decided nothing (positions ride as the payload)
     if ((rc = st_forward<1>(lc, T, p, b.r2, b.bk, b.bx, nullptr, nullptr, n, b.dcount + 1, 1, 2))) return rc;

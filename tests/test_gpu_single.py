@@ -546,3 +546,47 @@ def test_probe_start_matches_reference_hash_at_2g_slots(min_cap):
     assert (off == 0).mean() > 0.99
     del t
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("skew", ["super", "region"])
+def test_staged_overflowing_partition_areas(skew):
+    """Skewed batches overflow the staged schedule's fixed partition areas (csrc/staged.cu,
+    Part): a super-region holding most of the batch re-runs the exact level-1 partition,
+    and over-full regions hand their runs to the COPS kernels.  Statuses, values and
+    found flags match the direct probes."""
+    from paper_2009_07914_b200.probing import mix64_array
+    rng = np.random.default_rng(3 if skew == "super" else 4)
+    cap = 4_300_000
+    t = SingleValueHashTable(cap, layout="packed", key_bits=32, value_bits=32, group_width=8)
+    c = t.capacity
+    cand = np.unique(rng.integers(1, (1 << 32) - 3, size=12_000_000, dtype=np.uint64))
+    h = mix64_array(cand) % np.uint64(c)
+    if skew == "super":  # 90 % of the batch in super-region 0 (regions 0..255)
+        hot = cand[(h >> np.uint64(21)) == 0][:900_000]
+    else:  # three regions over-full, the rest uniform
+        hot = cand[np.isin(h >> np.uint64(13), [5, 6, 300])][:24_000]
+    cold = rng.permutation(cand[(h >> np.uint64(21)) != 0])[:100_000]
+    keys = np.concatenate([hot, cold, hot[:5000]])  # + in-batch duplicates
+    keys = keys[rng.permutation(keys.size)]
+    vals = rng.integers(0, 1 << 32, size=keys.size, dtype=np.uint64)
+    ref = SingleValueHashTable(cap, layout="packed", key_bits=32, value_bits=32, group_width=8)
+    ref.set_locality("off")
+    t.set_locality("staged")
+    st, st_ref = t.insert_device(keys, vals).cpu().numpy(), ref.insert_device(keys, vals).cpu().numpy()
+    assert t.occupied == ref.occupied == np.unique(keys).size
+    u, cnt = np.unique(keys, return_counts=True)
+    single = np.isin(keys, u[cnt == 1])
+    assert (st[single] == 0).all() and (st_ref[single] == 0).all()
+    ins = keys[st == 0]
+    assert np.unique(ins).size == ins.size == u.size  # every key inserted exactly once
+    absent = np.setdiff1d(cand[:200_000], keys)[:50_000]
+    q = np.concatenate([keys, absent])
+    v, f = t.retrieve_device(q)
+    vr, fr = ref.retrieve_device(q)
+    f, fr = f.cpu().numpy(), fr.cpu().numpy()
+    assert (f == fr).all() and f[:keys.size].all() and not f[keys.size:].any()
+    # values: the winner's value per key; both tables hold a value of one of the key's copies
+    vv = v.cpu().numpy().view(np.uint32)[:keys.size]
+    got = dict(zip(keys[single].tolist(), vv[single].tolist()))
+    want = dict(zip(keys[single].tolist(), vals[single].astype(np.uint32).tolist()))
+    assert got == want
