@@ -353,7 +353,8 @@ __global__ void __launch_bounds__(PT, CH_AB_SPLIT_MINB) k_st_split(TableRef T, u
   uint32_t* sP = sV + (VALS ? PTILE : 0);
   uint32_t* sR = sP + (POS ? PTILE : 0);
   uint16_t* sD = reinterpret_cast<uint16_t*>(sR + (RES ? PTILE : 0));
-  uint16_t* sL = sD + PTILE;  // level 2 only
+  uint16_t* sL = sD + PTILE;   // level 2 only: window start in bucketed order
+  uint16_t* sLi = sL + PTILE;  // level 2 only: window start in input order
   if (P.gate && *P.gate == 0) return;
   if (n_dev) n = *n_dev;
   __shared__ uint32_t hist[PBINS], boff[PBINS], gbase[PBINS], dbase[PBINS];
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(PT, CH_AB_SPLIT_MINB) k_st_split(TableRef T, u
     TileGeo g;
     if (!tile_geo<L>(t, n, P, s_sup, g)) break;  // tiles past the end are past it for every later t
     hist[threadIdx.x] = 0;  // PBINS == PT
-    uint32_t k[PI], v[PI], q[PI], w[PI], d[PI], r[PI];
+    uint32_t k[PI], v[PI], q[PI], w[PI], d[PI];  // d: bucket | rank << 16 (one register per item)
 #pragma unroll
     for (int it = 0; it < PI; ++it) {  // all loads in flight before any use
       const uint32_t li = (uint32_t)it * PT + threadIdx.x;
@@ -384,8 +385,8 @@ __global__ void __launch_bounds__(PT, CH_AB_SPLIT_MINB) k_st_split(TableRef T, u
       if (li >= g.cnt) continue;
       const uint32_t h = window_start(T, k[it], wj);
       const uint32_t b = L == 1 ? (h >> ST_LOG_R) >> ST_S2 : (h >> ST_LOG_R) - g.cbase;
-      r[it] = atomicAdd(&hist[b], 1u);
-      d[it] = b | (L == 2 ? (h & (ST_R - 1)) << 16 : 0u);  // window start rides along (registers)
+      d[it] = b | atomicAdd(&hist[b], 1u) << 16;
+      if (L == 2) sLi[li] = (uint16_t)(h & (ST_R - 1));  // the window start waits in shared memory
     }
     __syncthreads();
     const uint32_t hv = hist[threadIdx.x];
@@ -400,13 +401,13 @@ __global__ void __launch_bounds__(PT, CH_AB_SPLIT_MINB) k_st_split(TableRef T, u
       const uint32_t li = (uint32_t)it * PT + threadIdx.x;
       if (li >= g.cnt) continue;
       const uint32_t b = d[it] & 0xFFFFu;
-      const uint32_t j = boff[b] + r[it];
+      const uint32_t j = boff[b] + (d[it] >> 16);
       sK[j] = k[it];
       if (VALS) sV[j] = v[it];
       if (POS) sP[j] = q[it];
       if (RES) sR[j] = w[it];
       sD[j] = (uint16_t)b;
-      if (L == 2) sL[j] = (uint16_t)(d[it] >> 16);
+      if (L == 2) sL[j] = sLi[li];
       if (inv) inv[g.pos0 + li] = (uint16_t)j;
     }
     uint8_t mode = 0;
@@ -1025,7 +1026,7 @@ static int st_forward(const Launch& lc, const TableRef& T, const StPlan& p, Roun
   P.lim2 = r.lim2;
   P.flag = r.flag;
   P.ovf2 = r.ovf2;
-  const size_t sm1 = (size_t)PTILE * (4 + 4 * NPAY + 2), sm2 = sm1 + PTILE * 2;
+  const size_t sm1 = (size_t)PTILE * (4 + 4 * NPAY + 2), sm2 = sm1 + PTILE * 4;
   const unsigned t1 = (unsigned)p.tiles1, t2 = (unsigned)p.tiles2;
   auto k1f = k_st_split<1, NPAY>;
   auto k2f = k_st_split<2, NPAY>;
