@@ -634,6 +634,17 @@ __device__ __forceinline__ uint32_t lds32(const uint32_t* p) {
 constexpr uint32_t DBUF_B = 1024;  // window-full deferrals buffered per region (~4.6% of ~7.8K keys)
 constexpr uint32_t NONE = 0xffffffffu;
 
+// Lookups scan a byte per slot: 0 for the empty sentinel, 1..255 from the key word
+// otherwise, so a step reads 8 slots' fingerprints with three 4-byte loads instead of
+// eight key words (the random shared-memory gathers were the region pass's limit).
+constexpr uint32_t FP_BYTES = ((ST_R + ST_HALO + TILE_PAD + 16) + 15) & ~15u;
+__device__ __forceinline__ uint32_t slot_fp(uint32_t key, uint32_t e) {
+  if (key == e) return 0u;
+  const uint32_t f = (key * 0x9E3779B1u) >> 24;
+  return f ? f : 1u;
+}
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t v) { return (v - 0x01010101u) & ~v & 0x80808080u; }
+
 template <int MODE, bool R2>
 __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
                                                     const uint32_t* __restrict__ keys,
@@ -648,6 +659,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
   constexpr uint32_t OW = R2 ? WINDOW : 0u;  // sequence offset of the window probed here
   extern __shared__ __align__(128) unsigned char dsm[];
   uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
+  uint32_t* fp32 = reinterpret_cast<uint32_t*>(tile + ST_R + HALO + TILE_PAD);  // lookups: fingerprints
   __shared__ DeferBuf<INS, DBUF_B> B;  // -> DB
   __shared__ DeferBuf<INS, DBUF> BA;   // -> DA
   __shared__ uint32_t s_next;
@@ -694,6 +706,41 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
   // packed slot s: key word tw[2 s], value word tw[2 s + 1] (little-endian u64)
   uint32_t* const tw = reinterpret_cast<uint32_t*>(tile);
   auto step = [&](uint32_t k, uint32_t v, uint32_t lo, uint32_t ri, uint32_t& o) -> bool {
+    if constexpr (!INS) {  // fingerprints of 8 slots: decisive = the key's fingerprint or empty
+      const uint32_t x = lo + o, a = x >> 2, sh = (x & 3u) * 8u;
+      const uint32_t w0 = fp32[a], w1 = fp32[a + 1], w2 = fp32[a + 2];
+      const uint32_t b0 = __funnelshift_r(w0, w1, sh), b1 = __funnelshift_r(w1, w2, sh);
+      const uint32_t rep = slot_fp(k, e) * 0x01010101u;
+      // lowest flagged byte of each zero_bytes() is exact (false flags only sit above a true one)
+      uint64_t mk = (uint64_t)(zero_bytes(b0 ^ rep) | zero_bytes(b0)) |
+                    (uint64_t)(zero_bytes(b1 ^ rep) | zero_bytes(b1)) << 32;
+      const uint32_t room = WINDOW - o;
+      if (room < 8u) mk &= (1ull << (room * 8u)) - 1ull;
+      if (!mk) {
+        o += STEP;
+        if (o < WINDOW) return true;
+        defer_push(B, DB, k, v, ri, OW + WINDOW);  // window 0 has neither the key nor an empty
+        ndef += 1;
+        return false;
+      }
+      o += (uint32_t)(__ffsll((long long)mk) - 1) >> 3;
+      const uint32_t s2 = 2 * (lo + o);
+      const uint32_t c = tw[s2];
+      if (c != k && c != e) {  // fingerprint collision: scan on after it
+        o += 1;
+        if (o < WINDOW) return true;
+        defer_push(B, DB, k, v, ri, OW + WINDOW);
+        ndef += 1;
+        return false;
+      }
+      const bool hit = c == k;
+      res_val[ri] = hit ? tw[s2 + 1] : 0u;
+      res_flag[ri] = (uint8_t)hit;
+      ops += 1;
+      att += (long long)(OW + chunk_end(o, ug));
+      win += R2 ? 2 : 1;
+      return false;
+    } else {
     // key words only: a 4-byte gather per slot (the shared pipe is the kernel's limit)
     uint32_t w[STEP];
 #pragma unroll
@@ -749,6 +796,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
     att += (long long)(OW + chunk_end(o, ug));
     win += R2 ? 2 : 1;
     return false;
+    }
   };
 
   // key chunks: 32 consecutive keys of the region's list, one per lane
@@ -774,6 +822,17 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
   fetch(nbase, nk, nv, np, nl);
   uint32_t ptr = 0;  // entries of the current chunk handed out
   mbar_wait(&bar, 0);
+  if (!INS) {  // fingerprints of the staged slots (4 per word; slots past the halo are never decisive)
+    const uint32_t words = (len + HALO + TILE_PAD + 3) >> 2;
+    for (uint32_t i = threadIdx.x; i < words; i += RT) {
+      uint32_t f = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) f |= slot_fp(tw[2 * (4 * i + u)], e) << (8 * u);
+      fp32[i] = f;
+    }
+    for (uint32_t i = words + threadIdx.x; i < FP_BYTES / 4; i += RT) fp32[i] = 0xFFFFFFFFu;
+    __syncthreads();
+  }
 
   bool act = false;
   uint32_t k = 0, v = 0, lo = 0, ri = 0, o = 0;
@@ -839,7 +898,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
 
 template <int MODE, bool R2>
 constexpr size_t probe_smem() {
-  return (size_t)(ST_R + (MODE == 0 ? 0 : ST_HALO) + TILE_PAD) * 8;
+  return (size_t)(ST_R + (MODE == 0 ? 0 : ST_HALO) + TILE_PAD) * 8 + (MODE == 0 ? 0 : FP_BYTES);
 }
 
 // ------------------------------------------------------------- host side
