@@ -11,7 +11,7 @@
 // packed words) that its first window starts in.  One CTA then owns one region:
 // it stages the region in shared memory with one TMA bulk copy, resolves every
 // key of the region against it (the reference's window-0 rule, single_table.py:
-// 171-245 / 247-269, shared-memory 64-bit CAS for claims), and writes the region
+// 171-245 / 247-269, shared-memory CAS of the key word for claims), and writes the region
 // back with one bulk copy.  Every table byte crosses HBM once per batch, in 64 KiB
 // transfers; keys that window 0 cannot decide (window full, a tombstone before
 // the first empty, an insert window crossing the region end) are appended to a
@@ -20,10 +20,12 @@
 // batch, since nothing is ever removed from a table during an insert or lookup.
 //
 // Pipeline (all passes stream; n keys):
-//   count   region histogram of the keys                     k_st_count
-//   scan    region offsets (+ per-super-region L2 tile map)   prims.cu, k_st_plan
 //   L1      tile partition by super-region (256 regions)      k_st_split<1>
+//           into fixed areas; on overflow the exact count-based L1 is redone by
+//           gated kernels (count, scan, plan)                 k_st_count, k_st_plan
+//   plan    per-super-region L2 tile map                      k_st_plan_oa
 //   L2      tile partition by region, per super-region tiles  k_st_split<2>
+//           into fixed region areas; over-full runs -> the COPS kernels
 //   region  shared-memory probe of window 0                   k_st_probe
 //   rest    deferred keys through the COPS kernels            single.cu (n_dev, out_idx, o_start)
 //   back    results (status / value + found) to the caller's order: the inverse
