@@ -925,6 +925,13 @@ struct StPlan {
   uint64_t n1, n2, nres;    // level-1 / level-2 array lengths, region-order results (+ overflow)
 };
 
+// CH_STAGED_COUNT=1: the count-based partition for every batch (what batches of 2^30
+// keys and more use; the tests force it on small ones).
+static bool g_count_mode = [] {
+  const char* e = getenv("CH_STAGED_COUNT");
+  return e && e[0] == '1';
+}();
+
 // Overallocation: expected keys per region n R / c plus 6.25 % and 256 (> 8 standard
 // deviations of a uniform hash at the bench's 7.8 K keys per region), per super-region
 // + 3 % and one tile (> 40 deviations).  Skewed batches overflow and take the exact
@@ -935,7 +942,7 @@ static StPlan st_plan(const TableRef& T, uint64_t n) {
   p.supers = (p.regions + (1u << ST_S2) - 1) >> ST_S2;
   p.tiles1 = (n + PTILE - 1) / PTILE;
   p.tiles2 = p.tiles1 + p.supers;
-  p.oa = n < (1ull << 30);
+  p.oa = n < (1ull << 30) && !g_count_mode;
   const double per_region = (double)n * ST_R / (double)T.c;
   p.cs = p.oa ? (uint32_t)(per_region * (1u << ST_S2) * 1.03) + PTILE : 0u;
   p.cr = p.oa ? (((uint32_t)(per_region * 1.0625) + 256u + 63u) & ~63u) : 0u;  // regions start on 256 B key lines

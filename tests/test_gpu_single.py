@@ -491,9 +491,12 @@ def test_host_pipeline_matches_device_path():
     assert (dv.cpu().numpy().view(np.uint32) == v[:4096]).all()
 
 
-def test_staged_round2_and_fallback_caps_match_direct(tmp_path):
-    """The optional staged window-1 round (CH_STAGED_ROUND2=1) and a capped COPS pass
-    (CH_STAGED_FB_CTAS=1) give the same statuses / values / found flags as direct probes
+@pytest.mark.parametrize("switches", [{"CH_STAGED_ROUND2": "1", "CH_STAGED_FB_CTAS": "1"},
+                                      {"CH_STAGED_COUNT": "1"}])
+def test_staged_round2_and_fallback_caps_match_direct(tmp_path, switches):
+    """The optional staged window-1 round (CH_STAGED_ROUND2=1), a capped COPS pass
+    (CH_STAGED_FB_CTAS=1) and the count-based partition (CH_STAGED_COUNT=1, the path of
+    batches >= 2^30 keys) give the same statuses / values / found flags as direct probes
     (run in a child process: the switches are read when the library loads)."""
     import subprocess
     import sys
@@ -520,7 +523,7 @@ def test_staged_round2_and_fallback_caps_match_direct(tmp_path):
         "assert (a[1] == b[1]).all() and (a[2] == b[2]).all() and a[2][:n].all() and not a[2][n:].any()\n"
         "print('ok')\n")
     import os
-    env = dict(os.environ, CH_STAGED_ROUND2="1", CH_STAGED_FB_CTAS="1")
+    env = dict(os.environ, **switches)
     r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
