@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
   const uint32_t e = (uint32_t)T.e, t = (uint32_t)T.t;
   const uint32_t ug = (uint32_t)g;
   const uint32_t lane = threadIdx.x & 31u;
-  long long ops = 0, att = 0, win = 0, occ = 0, ndef = 0, nexc = 0;
+  uint32_t ops = 0, att = 0, win = 0, occ = 0, ndef = 0, nexc = 0;  // per thread: < 2^32 even for 2^32 keys
   bool claimed_any = false;
   const bool adj = t + 1u == e;  // default sentinels: "free" is one subtract and compare, (c - t) <= 1
 
@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
       res_val[ri] = hit ? tw[s2 + 1] : 0u;
       res_flag[ri] = (uint8_t)hit;
       ops += 1;
-      att += (long long)(OW + chunk_end(o, ug));
+      att += OW + chunk_end(o, ug);
       win += R2 ? 2 : 1;
       return false;
     } else {
@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
       res_flag[ri] = (uint8_t)hit;
     }
     ops += 1;
-    att += (long long)(OW + chunk_end(o, ug));
+    att += OW + chunk_end(o, ug);
     win += R2 ? 2 : 1;
     return false;
     }
@@ -905,7 +905,8 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
     __syncthreads();
     if (threadIdx.x == 0 && dirty) bulk_store_wait(slots + rbase, tile, len * 8u);
   }
-  const long long cv6[6] = {ops, att, win, occ, nexc, ndef};
+  const long long cv6[6] = {(long long)ops, (long long)att, (long long)win, (long long)occ, (long long)nexc,
+                            (long long)ndef};
   long long* const dst[6] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
                              &T.ctr->occupied, INS ? (long long*)exc : nullptr, (long long*)&T.ctr->deferred};
   cta_add<6>(cv6, dst);
