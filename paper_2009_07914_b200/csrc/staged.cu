@@ -331,6 +331,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // round-1 position of a round-2 key, or of a lookup key in round 2 with NPAY=1
 // meaning the position).  Round 2 (wj = 1) partitions the deferred keys by their
 // window-1 start; its count lives on the device (n_dev) and it needs no inverse.
+#ifndef CH_AB_P0_MINB
+#define CH_AB_P0_MINB 4  // level 1 of lookup keys: 4 CTAs/SM without spills (0.98 -> 0.95 ms)
+#endif
 #ifndef CH_AB_L2P_MINB
 #define CH_AB_L2P_MINB 2  // level 2 with payloads: no spills at 2 CTAs/SM (1.83 -> 1.72 ms)
 #endif
@@ -338,7 +341,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define CH_AB_SPLIT_MINB 3  // 3 CTAs per SM (<= 42 registers, small spills): 26.5 -> 27.1 G ops/s
 #endif
 template <int L, int NPAY>
-__global__ void __launch_bounds__(PT, (L == 2 && NPAY >= 1) ? CH_AB_L2P_MINB : CH_AB_SPLIT_MINB) k_st_split(TableRef T, uint64_t n, Part P, uint32_t supers,
+__global__ void __launch_bounds__(PT, (L == 2 && NPAY >= 1) ? CH_AB_L2P_MINB : (L == 1 && NPAY == 0) ? CH_AB_P0_MINB : CH_AB_SPLIT_MINB) k_st_split(TableRef T, uint64_t n, Part P, uint32_t supers,
                                                     uint32_t ntiles,
                                                     const uint32_t* __restrict__ kin,
                                                     const uint32_t* __restrict__ vin,
