@@ -43,8 +43,11 @@ enum Outcome : int { OUT_NONE = -1, OUT_CLAIMED = 0, OUT_FOUND = 1, OUT_FULL = 2
 template <typename K, typename V, int MODE>
 constexpr int insert_chunk() { return MODE == 1 ? 1024 : chunk_for<K, V>(); }
 
+#ifndef CH_AB_PROBE_MINB
+#define CH_AB_PROBE_MINB 4  // 5 (<= 51 registers) measured slower for the staged fallback (2.14 -> 2.43 ms)
+#endif
 template <Layout LAY, typename K, typename V, int G, int MODE>
-__global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restrict__ keys,
+__global__ void __launch_bounds__(256, CH_AB_PROBE_MINB) k_insert(TableRef T, const K* __restrict__ keys,
                                                 const V* __restrict__ vals, uint64_t n,
                                                 uint8_t* __restrict__ status,
                                                 int64_t* __restrict__ slot_out,
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(256, 4) k_insert(TableRef T, const K* __restri
 // the first 128 B of window 0 (FastSpan); the rest are queued and finished by
 // the flattened general loop.
 template <Layout LAY, typename K, typename V, int G, int MODE>
-__global__ void __launch_bounds__(256, 4) k_lookup(TableRef T, const K* __restrict__ keys, uint64_t n,
+__global__ void __launch_bounds__(256, CH_AB_PROBE_MINB) k_lookup(TableRef T, const K* __restrict__ keys, uint64_t n,
                                                 V* __restrict__ vals_out, uint8_t* __restrict__ flag,
                                                 int64_t* __restrict__ slot_out,
                                                 uint32_t* __restrict__ att_out,
