@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
       const uint32_t x = lo + o, a = x >> 2, sh = (x & 3u) * 8u;
       const uint32_t w0 = fp32[a], w1 = fp32[a + 1], w2 = fp32[a + 2];
       const uint32_t b0 = __funnelshift_r(w0, w1, sh), b1 = __funnelshift_r(w1, w2, sh);
-      const uint32_t rep = slot_fp(k, e) * 0x01010101u;
+      const uint32_t rep = v;  // lookups carry the key's fingerprint in every byte of v
       // lowest flagged byte of each zero_bytes() is exact (false flags only sit above a true one)
       uint64_t mk = (uint64_t)(zero_bytes(b0 ^ rep) | zero_bytes(b0)) |
                     (uint64_t)(zero_bytes(b1 ^ rep) | zero_bytes(b1)) << 32;
@@ -856,6 +856,7 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
   }
 
   bool act = false;
+  const uint32_t k0u = (uint32_t)k0;  // positions stay below 2^32 (staged_supported)
   uint32_t k = 0, v = 0, lo = 0, ri = 0, o = 0;
   for (;;) {
     const unsigned need = __ballot_sync(0xffffffffu, !act);
@@ -881,8 +882,9 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
         fetch(nbase, nk, nv, np, nl);
       }
       if (got) {
-        k = xk, v = xv, lo = xl, o = 0;
-        ri = R2 ? xp : (uint32_t)(k0 + tb + src);
+        k = xk, lo = xl, o = 0;
+        v = INS ? xv : slot_fp(xk, e) * 0x01010101u;
+        ri = R2 ? xp : k0u + tb + src;
         if (k == e || k == t) {  // sentinels are never stored (single_table.py:369-370, 391-393)
           if (INS) {
             status[ri] = ST_INVALID;
