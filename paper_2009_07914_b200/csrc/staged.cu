@@ -645,7 +645,11 @@ constexpr uint32_t NONE = 0xffffffffu;
 // Lookups scan a byte per slot: 0 for the empty sentinel, 1..255 from the key word
 // otherwise, so a step reads 8 slots' fingerprints with three 4-byte loads instead of
 // eight key words (the random shared-memory gathers were the region pass's limit).
-constexpr uint32_t FP_BYTES = ((ST_R + ST_HALO + TILE_PAD + 16) + 15) & ~15u;
+#ifndef CH_AB_FSTEP
+#define CH_AB_FSTEP 16
+#endif
+constexpr uint32_t FSTEP = CH_AB_FSTEP;  // slots per lookup step (multiple of 8)
+constexpr uint32_t FP_BYTES = ((ST_R + ST_HALO + TILE_PAD + FSTEP + 16) + 15) & ~15u;
 __device__ __forceinline__ uint32_t slot_fp(uint32_t key, uint32_t e) {
   if (key == e) return 0u;
   const uint32_t f = (key * 0x9E3779B1u) >> 24;
@@ -714,24 +718,34 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
   // packed slot s: key word tw[2 s], value word tw[2 s + 1] (little-endian u64)
   uint32_t* const tw = reinterpret_cast<uint32_t*>(tile);
   auto step = [&](uint32_t k, uint32_t v, uint32_t lo, uint32_t ri, uint32_t& o) -> bool {
-    if constexpr (!INS) {  // fingerprints of 8 slots: decisive = the key's fingerprint or empty
+    if constexpr (!INS) {  // fingerprints of FSTEP slots: decisive = the key's fingerprint or empty
       const uint32_t x = lo + o, a = x >> 2, sh = (x & 3u) * 8u;
-      const uint32_t w0 = fp32[a], w1 = fp32[a + 1], w2 = fp32[a + 2];
-      const uint32_t b0 = __funnelshift_r(w0, w1, sh), b1 = __funnelshift_r(w1, w2, sh);
       const uint32_t rep = v;  // lookups carry the key's fingerprint in every byte of v
+      uint32_t wv[FSTEP / 4 + 1];
+#pragma unroll
+      for (int q = 0; q <= (int)FSTEP / 4; ++q) wv[q] = fp32[a + q];
       // lowest flagged byte of each zero_bytes() is exact (false flags only sit above a true one)
-      uint64_t mk = (uint64_t)(zero_bytes(b0 ^ rep) | zero_bytes(b0)) |
-                    (uint64_t)(zero_bytes(b1 ^ rep) | zero_bytes(b1)) << 32;
+      uint64_t mk[FSTEP / 8];
+#pragma unroll
+      for (int q = 0; q < (int)FSTEP / 8; ++q) {
+        const uint32_t b0 = __funnelshift_r(wv[2 * q], wv[2 * q + 1], sh);
+        const uint32_t b1 = __funnelshift_r(wv[2 * q + 1], wv[2 * q + 2], sh);
+        mk[q] = (uint64_t)(zero_bytes(b0 ^ rep) | zero_bytes(b0)) |
+                (uint64_t)(zero_bytes(b1 ^ rep) | zero_bytes(b1)) << 32;
+      }
       const uint32_t room = WINDOW - o;
-      if (room < 8u) mk &= (1ull << (room * 8u)) - 1ull;
-      if (!mk) {
-        o += STEP;
+      uint32_t u = FSTEP;
+#pragma unroll
+      for (int q = (int)FSTEP / 8 - 1; q >= 0; --q)
+        if (mk[q]) u = 8u * q + ((uint32_t)(__ffsll((long long)mk[q]) - 1) >> 3);
+      if (u >= room) {  // nothing decisive inside the window's remaining slots
+        o += FSTEP;
         if (o < WINDOW) return true;
         defer_push(B, DB, k, v, ri, OW + WINDOW);  // window 0 has neither the key nor an empty
         ndef += 1;
         return false;
       }
-      o += (uint32_t)(__ffsll((long long)mk) - 1) >> 3;
+      o += u;
       const uint32_t s2 = 2 * (lo + o);
       const uint32_t c = tw[s2];
       if (c != k && c != e) {  // fingerprint collision: scan on after it
