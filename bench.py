@@ -241,6 +241,47 @@ def cpu_run(n: int, load: float, steps: int, warmup: int, threads: int):
     return 2 * n / (sum(times) / len(times)) / 1e9, times
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def python_reference_rate(n: int, load: float):
+    """The UNMODIFIED reference package (pure Python, installed into baseline/_ref with
+    pip --target) on a small sample of the same workload: SingleValueHashTable packed
+    32|32, g = 8, insert_bulk + retrieve_bulk, one thread (its thread pool gives no
+    speed-up: GIL).  Informational next to the C restatement the arm times."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "coophash")):
+        return None
+    import numpy as np
+    sys.path.insert(0, ref)
+    try:
+        from coophash import SingleValueHashTable as RefTable
+    finally:
+        sys.path.remove(ref)
+    rng = np.random.default_rng(42)
+    keys = rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=n + n // 8 + 16,
+                                                  dtype=np.uint64)))[:n].tolist()
+    vals = list(range(1, n + 1))
+    t = RefTable(math.ceil(n / load), layout="packed", key_bits=32, value_bits=32, group_width=G_DEFAULT)
+    t0 = time.perf_counter()
+    t.insert_bulk(list(zip(keys, vals)))
+    got = t.retrieve_bulk(keys)
+    dt = time.perf_counter() - t0
+    if got != vals:
+        raise SystemExit("python reference verification failed")
+    return {"value": 2 * n / dt / 1e9, "unit": "G ops/s", "cores": 1, "kind": "reference",
+            "sample": f"{n} unique keys insert + retrieve at load {load} (coophash from baseline/_ref)",
+            "seconds": dt}
+
+
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -248,6 +289,10 @@ def run_reference(args) -> None:
     threads = os.cpu_count() or 1
     n = args.cpu_n
     value, times = cpu_run(n, args.load, args.steps, args.warmup, threads)
+    try:
+        pyref = python_reference_rate(1 << 16, args.load)
+    except Exception as err:  # informational only
+        pyref = {"error": repr(err)}
     line = {
         "metric": METRIC, "value": value, "unit": "G ops/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -258,13 +303,28 @@ def run_reference(args) -> None:
                    "note": "CPU: oracle/ C restatement of the reference algorithm (the Python "
                            "reference cannot travel to the box); bounded sample of the workload"},
         "cpu_baseline": {"value": value, "unit": "G ops/s", "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{n} unique keys insert + retrieve at load {args.load}, per step"},
         "e2e": {"value": value, "unit": "G ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_python": pyref,
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ GPU arm
+
+def relaunch(gpus: int) -> None:
+    """`python bench.py --gpus N` outside torchrun: re-run this command as N ranks, one per
+    GPU, on one node (torch.distributed.run, rendezvous on 127.0.0.1)."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
 
 def main() -> None:
     ap = argparse.ArgumentParser()
@@ -286,6 +346,8 @@ def main() -> None:
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args.gpus)  # one process per GPU (torchrun, NCCL); does not return
 
     import torch
     import torch.distributed as dist
@@ -295,6 +357,9 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU "
+                         "(python bench.py --gpus N re-launches itself under torchrun)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -462,7 +527,7 @@ def main() -> None:
         if world == 1 and not args.no_cpu:
             threads = os.cpu_count() or 1
             cv, _ = cpu_run(args.cpu_n, args.load, 1, 1, threads)
-            cpu = {"value": cv, "unit": "G ops/s", "cores": threads, "kind": "port",
+            cpu = {"value": cv, "unit": "G ops/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                    "sample": f"{args.cpu_n} unique keys, insert + retrieve at load {args.load} "
                              "(oracle/ C restatement, OpenMP)"}
         line = {

@@ -85,6 +85,7 @@ int ch_create(ch_table** out, const ch_config* cfg);
 int ch_destroy(ch_table* t);
 int ch_clear(ch_table* t, void* stream);               /* K0: every cell empty, counters 0 */
 int ch_get_stats(ch_table* t, ch_stats* out);          /* synchronizes the table's work */
+int ch_get_config(ch_table* t, ch_config* out);        /* the resolved configuration (max_outer_attempts set) */
 int ch_reset_probe_counters(ch_table* t, void* stream); /* single_table.py:136-138 */
 int ch_synchronize(ch_table* t);
 /* schedule of big bulk insert / retrieve batches: 0 auto (table > 256 MiB and n >= c/16:
@@ -187,6 +188,38 @@ int ch_gather(const void* d_src, int elem_bytes, const uint64_t* d_perm, uint64_
 int ch_segment_copy(const void* d_src, int elem_bytes, const uint64_t* d_src_off,
                     const uint64_t* d_idx, uint64_t n, const uint64_t* d_dst_off, void* d_dst,
                     int device, void* stream);
+
+/* ---- distributed single-value table over the devices of one process ----
+ * replaces DistributedTable(num_shards, shard_factory, mode=DISTRIBUTED) with
+ * single-value shards (distributed.py:84-178): key k lives on shard
+ * (mix64(k) >> 32) mod S (distributed.py:44-45).  The shards are ordinary tables
+ * made by ch_create (one per device for NCCL; several may share a device with the
+ * copy transport); the handle does not own them.  A bulk call takes one batch per
+ * source s (device of shards[s], stream streams[s]; n[s] may be 0): route + stable
+ * split on the source, segments to their shards (NCCL grouped send/recv over NVLink,
+ * or the copy engines), the shard's ch_insert / ch_retrieve, results back, inverse
+ * permutation into the source's order.  One host synchronisation per call (the
+ * segment sizes); everything else is stream-ordered on streams[]. */
+typedef struct ch_dist ch_dist;
+enum { CH_DIST_AUTO = 0, CH_DIST_NCCL = 1, CH_DIST_COPY = 2 };
+int ch_dist_create(ch_dist** out, ch_table* const* shards, int num_shards, int transport);
+int ch_dist_destroy(ch_dist* d);
+int ch_dist_info(ch_dist* d, int* num_shards, int* transport);
+/* insert_bulk (distributed.py:131-147): d_status[s][n[s]] InsertStatus codes */
+int ch_dist_insert(ch_dist* d, const void* const* d_keys, const void* const* d_vals, const uint64_t* n,
+                   uint8_t* const* d_status, void* const* streams);
+/* retrieve_bulk, distributed mode (distributed.py:151-178): values + found flags */
+int ch_dist_retrieve(ch_dist* d, const void* const* d_keys, const uint64_t* n, void* const* d_vals_out,
+                     uint8_t* const* d_found, void* const* streams);
+
+/* ---- u32-permutation variants (batches < 2^32): half the index traffic of the u64 forms ---- */
+int ch_multi_split32(const void* d_keys, int key_bytes, const void* d_vals, int val_bytes, uint64_t n,
+                     uint32_t shards, uint32_t* d_perm, uint64_t* d_offsets, void* d_keys_out, void* d_vals_out,
+                     int device, void* stream);
+int ch_scatter32(const void* d_src, int elem_bytes, const uint32_t* d_perm, uint64_t n, void* d_dst, int device,
+                 void* stream);
+int ch_gather32(const void* d_src, int elem_bytes, const uint32_t* d_perm, uint64_t n, void* d_dst, int device,
+                void* stream);
 
 #ifdef __cplusplus
 }

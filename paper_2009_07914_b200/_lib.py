@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("CH_LIB_PATH") or os.path.join(_HERE, "libcoophash_b20
 CH_OK, CH_EINVAL, CH_ENOMEM, CH_EIO, CH_ETIMEDOUT = 0, -22, -12, -5, -110
 CH_SINGLE, CH_MULTI, CH_BUCKET = 0, 1, 2
 CH_SOA, CH_AOS, CH_PACKED = 0, 1, 2
+CH_DIST_AUTO, CH_DIST_NCCL, CH_DIST_COPY = 0, 1, 2
 
 
 class ch_config(C.Structure):
@@ -79,6 +80,18 @@ _SIGS = {
     "ch_scatter": (C.c_int, [_P, C.c_int, _P, _U64, _P, C.c_int, _P]),
     "ch_gather": (C.c_int, [_P, C.c_int, _P, _U64, _P, C.c_int, _P]),
     "ch_segment_copy": (C.c_int, [_P, C.c_int, _P, _P, _U64, _P, _P, C.c_int, _P]),
+    "ch_get_config": (C.c_int, [_P, C.POINTER(ch_config)]),
+    "ch_dist_create": (C.c_int, [C.POINTER(_P), C.POINTER(_P), C.c_int, C.c_int]),
+    "ch_dist_destroy": (C.c_int, [_P]),
+    "ch_dist_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ch_dist_insert": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_U64), C.POINTER(_P),
+                                 C.POINTER(_P)]),
+    "ch_dist_retrieve": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_U64), C.POINTER(_P), C.POINTER(_P),
+                                   C.POINTER(_P)]),
+    "ch_multi_split32": (C.c_int, [_P, C.c_int, _P, C.c_int, _U64, C.c_uint32, _P, _P, _P, _P,
+                                   C.c_int, _P]),
+    "ch_scatter32": (C.c_int, [_P, C.c_int, _P, _U64, _P, C.c_int, _P]),
+    "ch_gather32": (C.c_int, [_P, C.c_int, _P, _U64, _P, C.c_int, _P]),
 }
 
 _lib = None

@@ -27,8 +27,10 @@ void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxe
 // prims.cu / bucket.cu entry points
 int mix64_array(const Launch& lc, const uint64_t* in, uint64_t n, uint64_t seed, uint64_t* out);
 int multi_split(const Launch& lc, const void* keys, int kbytes, const void* vals, int vbytes, uint64_t n,
-                uint32_t shards, uint64_t* perm, uint64_t* offsets, void* keys_out, void* vals_out, void* scratch,
-                size_t scratch_bytes);
+                uint32_t shards, void* perm, int perm_bytes, uint64_t* offsets, void* keys_out, void* vals_out,
+                void* scratch, size_t scratch_bytes);
+int permute32(const Launch& lc, const void* src, int elem_bytes, const uint32_t* perm, uint64_t n, void* dst,
+              bool scatter);
 size_t split_scratch_bytes(uint64_t n, uint32_t shards);
 int permute(const Launch& lc, const void* src, int elem_bytes, const uint64_t* perm, uint64_t n, void* dst,
             bool scatter);
@@ -500,6 +502,12 @@ int ch_get_stats(ch_table* t, ch_stats* out) {
   return CH_OK;
 }
 
+int ch_get_config(ch_table* t, ch_config* out) {
+  if (!t || !out) return fail(CH_EINVAL, "null argument");
+  *out = t->cfg;
+  return CH_OK;
+}
+
 int ch_reset_probe_counters(ch_table* t, void* stream) {
   if (!t) return fail(CH_EINVAL, "null table");
   Ordered o(t, stream);
@@ -814,8 +822,8 @@ int ch_multi_split(const void* keys, int key_bytes, const void* vals, int val_by
   const size_t sb = split_scratch_bytes(n, shards);
   void* p = sc.get(sb);
   if (!p) return fail(CH_ENOMEM, "scratch allocation failed");
-  return multi_split(lc, keys, key_bytes, vals, vals ? val_bytes : 4, n, shards, perm, offsets, keys_out, vals_out,
-                     p, sb);
+  return multi_split(lc, keys, key_bytes, vals, vals ? val_bytes : 4, n, shards, perm, 8, offsets, keys_out,
+                     vals_out, p, sb);
 }
 
 int ch_partition(const uint32_t* dest, uint64_t n, uint32_t shards, uint64_t* perm, uint64_t* offsets, int device,
@@ -827,7 +835,36 @@ int ch_partition(const uint32_t* dest, uint64_t n, uint32_t shards, uint64_t* pe
   const size_t sb = split_scratch_bytes(n, shards);
   void* p = sc.get(sb);
   if (!p) return fail(CH_ENOMEM, "scratch allocation failed");
-  return multi_split(lc, dest, 0, nullptr, 4, n, shards, perm, offsets, nullptr, nullptr, p, sb);
+  return multi_split(lc, dest, 0, nullptr, 4, n, shards, perm, 8, offsets, nullptr, nullptr, p, sb);
+}
+
+int ch_multi_split32(const void* keys, int key_bytes, const void* vals, int val_bytes, uint64_t n, uint32_t shards,
+                     uint32_t* perm, uint64_t* offsets, void* keys_out, void* vals_out, int device, void* stream) {
+  if (!offsets || (n && (!keys || !perm))) return fail(CH_EINVAL, "null buffer");
+  if (key_bytes != 4 && key_bytes != 8) return fail(CH_EINVAL, "key_bytes must be 4 or 8");
+  if (vals && val_bytes != 4 && val_bytes != 8) return fail(CH_EINVAL, "val_bytes must be 4 or 8");
+  DeviceGuard dev(device);
+  Launch lc = plain_launch(device, stream);
+  Scratch sc(lc.stream);
+  const size_t sb = split_scratch_bytes(n, shards);
+  void* p = sc.get(sb);
+  if (!p) return fail(CH_ENOMEM, "scratch allocation failed");
+  return multi_split(lc, keys, key_bytes, vals, vals ? val_bytes : 4, n, shards, perm, 4, offsets, keys_out,
+                     vals_out, p, sb);
+}
+
+int ch_scatter32(const void* src, int elem_bytes, const uint32_t* perm, uint64_t n, void* dst, int device,
+                 void* stream) {
+  if (n && (!src || !perm || !dst)) return fail(CH_EINVAL, "null buffer");
+  DeviceGuard dev(device);
+  return permute32(plain_launch(device, stream), src, elem_bytes, perm, n, dst, true);
+}
+
+int ch_gather32(const void* src, int elem_bytes, const uint32_t* perm, uint64_t n, void* dst, int device,
+                void* stream) {
+  if (n && (!src || !perm || !dst)) return fail(CH_EINVAL, "null buffer");
+  DeviceGuard dev(device);
+  return permute32(plain_launch(device, stream), src, elem_bytes, perm, n, dst, false);
 }
 
 int ch_scatter(const void* src, int elem_bytes, const uint64_t* perm, uint64_t n, void* dst, int device,

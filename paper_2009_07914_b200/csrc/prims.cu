@@ -185,12 +185,12 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const K* __restri
 }
 
 // stable scatter: rounds in input order, ranks within a round by warp then lane
-template <typename K, typename V>
+template <typename K, typename V, typename PI_T>
 __global__ void __launch_bounds__(SPLIT_THREADS) k_split_scatter(const K* __restrict__ keys,
                                                                 const V* __restrict__ vals, uint64_t n,
                                                                 uint32_t shards,
                                                                 const uint64_t* __restrict__ hist_off,
-                                                                uint64_t* __restrict__ perm,
+                                                                PI_T* __restrict__ perm,
                                                                 K* __restrict__ keys_out,
                                                                 V* __restrict__ vals_out) {
   constexpr int NW = SPLIT_THREADS / 32;
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_scatter(const K* __rest
     if (valid) {
       uint64_t pos = run[d] + rank;
       for (int w = 0; w < warp; ++w) pos += wcnt[w][d];
-      perm[pos] = i;
+      perm[pos] = (PI_T)i;
       if (keys_out) keys_out[pos] = key;
       if (vals_out) vals_out[pos] = vals[i];
     }
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_scatter(const K* __rest
 __global__ void k_split_offsets(const uint64_t* __restrict__ hist_off, uint32_t shards, uint64_t tiles,
                                 uint64_t n, uint64_t* __restrict__ offsets) {
   for (uint32_t d = threadIdx.x; d <= shards; d += blockDim.x)
-    offsets[d] = d == shards ? n : hist_off[(uint64_t)d * tiles];
+    offsets[d] = d == shards ? n : (hist_off ? hist_off[(uint64_t)d * tiles] : 0);  // n == 0: no tiles
 }
 
 size_t split_scratch_bytes(uint64_t n, uint32_t shards) {
@@ -245,9 +245,9 @@ size_t split_scratch_bytes(uint64_t n, uint32_t shards) {
   return h * 4 + (h + 1) * 8 + scan_words_needed(h) * 8 + 256;
 }
 
-template <typename K, typename V>
+template <typename K, typename V, typename PI_T>
 static int split_impl(const Launch& lc, const K* keys, const V* vals, uint64_t n, uint32_t shards,
-                      uint64_t* perm, uint64_t* offsets, K* keys_out, V* vals_out, void* scratch,
+                      PI_T* perm, uint64_t* offsets, K* keys_out, V* vals_out, void* scratch,
                       size_t scratch_bytes) {
   const uint64_t tiles = (n + SPLIT_TILE - 1) / SPLIT_TILE;
   if (n == 0) {
@@ -270,7 +270,7 @@ static int split_impl(const Launch& lc, const K* keys, const V* vals, uint64_t n
   if (rc) return rc;
   rc = exclusive_scan_u32(lc, hist, h, hist_off, scan_scratch, scratch_bytes - used);
   if (rc) return rc;
-  k_split_scatter<K, V><<<(unsigned)tiles, SPLIT_THREADS, 0, lc.stream>>>(keys, vals, n, shards, hist_off, perm,
+  k_split_scatter<K, V, PI_T><<<(unsigned)tiles, SPLIT_THREADS, 0, lc.stream>>>(keys, vals, n, shards, hist_off, perm,
                                                                          keys_out, vals_out);
   count_launch();
   rc = cuda_check(cudaGetLastError(), "split scatter");
@@ -281,16 +281,27 @@ static int split_impl(const Launch& lc, const K* keys, const V* vals, uint64_t n
 }
 
 int multi_split(const Launch& lc, const void* keys, int kbytes, const void* vals, int vbytes, uint64_t n,
-                uint32_t shards, uint64_t* perm, uint64_t* offsets, void* keys_out, void* vals_out, void* scratch,
-                size_t scratch_bytes) {
+                uint32_t shards, void* perm, int perm_bytes, uint64_t* offsets, void* keys_out, void* vals_out,
+                void* scratch, size_t scratch_bytes) {
+  if (perm_bytes != 4 && perm_bytes != 8) {
+    set_error("perm_bytes must be 4 or 8");
+    return -22;
+  }
+  if (perm_bytes == 4 && n > 0xFFFFFFFFull) {
+    set_error("32-bit permutations need n < 2^32");
+    return -22;
+  }
   if (shards < 1 || shards > SPLIT_MAX_SHARDS) {
     set_error("shards must be in [1, 256]");
     return -22;
   }
   if (!vals) vals_out = nullptr;
 #define CHB_SPLIT(K, V)                                                                                  \
-  return split_impl<K, V>(lc, (const K*)keys, (const V*)vals, n, shards, perm, offsets, (K*)keys_out, \
-                          (V*)vals_out, scratch, scratch_bytes);
+  return perm_bytes == 4                                                                                 \
+             ? split_impl<K, V, uint32_t>(lc, (const K*)keys, (const V*)vals, n, shards, (uint32_t*)perm,   \
+                                          offsets, (K*)keys_out, (V*)vals_out, scratch, scratch_bytes)     \
+             : split_impl<K, V, uint64_t>(lc, (const K*)keys, (const V*)vals, n, shards, (uint64_t*)perm,   \
+                                          offsets, (K*)keys_out, (V*)vals_out, scratch, scratch_bytes);
   if (kbytes == 0) CHB_SPLIT(DestGiven, uint32_t)
   if (kbytes == 4 && vbytes == 4) CHB_SPLIT(uint32_t, uint32_t)
   if (kbytes == 4 && vbytes == 8) CHB_SPLIT(uint32_t, uint64_t)
@@ -302,8 +313,8 @@ int multi_split(const Launch& lc, const void* keys, int kbytes, const void* vals
 }
 
 // ------------------------------------------------- scatter / gather / copy
-template <typename X, bool SCATTER>
-__global__ void k_permute(const X* __restrict__ src, const uint64_t* __restrict__ perm, uint64_t n,
+template <typename X, bool SCATTER, typename PI_T>
+__global__ void k_permute(const X* __restrict__ src, const PI_T* __restrict__ perm, uint64_t n,
                           X* __restrict__ dst) {
   const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -312,17 +323,18 @@ __global__ void k_permute(const X* __restrict__ src, const uint64_t* __restrict_
   }
 }
 
-int permute(const Launch& lc, const void* src, int elem_bytes, const uint64_t* perm, uint64_t n, void* dst,
-            bool scatter) {
+template <typename PI_T>
+static int permute_impl(const Launch& lc, const void* src, int elem_bytes, const PI_T* perm, uint64_t n, void* dst,
+                        bool scatter) {
 #define CHB_PERM(X)                                                                                       \
   {                                                                                                       \
     if (scatter) {                                                                                        \
-      auto kern = k_permute<X, true>;                                                                     \
+      auto kern = k_permute<X, true, PI_T>;                                                               \
       return launch_persistent(lc, (const void*)kern, n, 1, [&](dim3 g, dim3 b) {                        \
         kern<<<g, b, 0, lc.stream>>>((const X*)src, perm, n, (X*)dst);                                    \
       });                                                                                                 \
     }                                                                                                     \
-    auto kern = k_permute<X, false>;                                                                      \
+    auto kern = k_permute<X, false, PI_T>;                                                                \
     return launch_persistent(lc, (const void*)kern, n, 1,                                                 \
                              [&](dim3 g, dim3 b) { kern<<<g, b, 0, lc.stream>>>((const X*)src, perm, n, (X*)dst); }); \
   }
@@ -334,6 +346,15 @@ int permute(const Launch& lc, const void* src, int elem_bytes, const uint64_t* p
 #undef CHB_PERM
   set_error("elem_bytes must be 1, 4 or 8");
   return -22;
+}
+
+int permute(const Launch& lc, const void* src, int elem_bytes, const uint64_t* perm, uint64_t n, void* dst,
+            bool scatter) {
+  return permute_impl<uint64_t>(lc, src, elem_bytes, perm, n, dst, scatter);
+}
+int permute32(const Launch& lc, const void* src, int elem_bytes, const uint32_t* perm, uint64_t n, void* dst,
+              bool scatter) {
+  return permute_impl<uint32_t>(lc, src, elem_bytes, perm, n, dst, scatter);
 }
 
 template <typename X>

@@ -84,6 +84,32 @@ def split_device(keys: torch.Tensor, num_shards: int, values: torch.Tensor | Non
     return perm, offsets, kout, vout
 
 
+def split_device32(keys: torch.Tensor, num_shards: int, values: torch.Tensor | None = None, stream=None):
+    """split_device with a u32 permutation (ch_multi_split32): batches < 2^32 keys.
+
+    Returns (perm int32[n] holding u32 source indices, offsets int64[S+1], keys_out, values_out)."""
+    dev = keys.device.index
+    n = keys.numel()
+    perm = torch.empty(n, dtype=torch.int32, device=keys.device)
+    offsets = torch.empty(num_shards + 1, dtype=torch.int64, device=keys.device)
+    kout = torch.empty_like(keys)
+    vout = torch.empty_like(values) if values is not None else None
+    _lib.check(_lib.lib().ch_multi_split32(
+        keys.data_ptr(), keys.element_size(), values.data_ptr() if values is not None else None,
+        values.element_size() if values is not None else 4, n, num_shards, perm.data_ptr(), offsets.data_ptr(),
+        kout.data_ptr(), vout.data_ptr() if vout is not None else None, dev,
+        _io.stream_of(dev, stream)), "multi_split32")
+    return perm, offsets, kout, vout
+
+
+def scatter_device32(src: torch.Tensor, perm: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """out[perm[i]] = src[i] with a u32 permutation (ch_scatter32)."""
+    dev = src.device.index
+    _lib.check(_lib.lib().ch_scatter32(src.data_ptr(), src.element_size(), perm.data_ptr(), src.numel(),
+                                       out.data_ptr(), dev, _io.stream_of(dev, stream)), "scatter32")
+    return out
+
+
 def scatter_device(src: torch.Tensor, perm: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
     """out[perm[i]] = src[i] (ch_scatter)."""
     dev = src.device.index
@@ -131,6 +157,83 @@ def _is_multi(table) -> bool:
     return hasattr(table, "count_bulk")
 
 
+class NativeDist:
+    """ch_dist_* (include/coophash_b200.h): the distributed single-value table in the C ABI.
+
+    Wraps existing single-value shard tables (one per device: NCCL grouped send/recv over
+    NVLink; shards sharing a device: copy engines).  ``insert`` / ``retrieve`` take one batch
+    per source shard (``None`` = no keys from that source) and return per-source results,
+    each on its source's device (distributed.py:131-178)."""
+
+    TRANSPORTS = {"auto": _lib.CH_DIST_AUTO, "nccl": _lib.CH_DIST_NCCL, "copy": _lib.CH_DIST_COPY}
+
+    def __init__(self, shards: Sequence, transport: str = "auto"):
+        import ctypes as C
+        self.shards = list(shards)
+        S = len(self.shards)
+        arr = (C.c_void_p * S)(*[t._dt.handle for t in self.shards])
+        h = C.c_void_p()
+        _lib.check(_lib.lib().ch_dist_create(C.byref(h), arr, S, self.TRANSPORTS[transport]), "dist_create")
+        self.handle = h
+        ns, tr = C.c_int(), C.c_int()
+        _lib.check(_lib.lib().ch_dist_info(h, C.byref(ns), C.byref(tr)), "dist_info")
+        self.transport = {v: k for k, v in self.TRANSPORTS.items()}[tr.value]
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _lib.lib().ch_dist_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ptrs(self, ts):
+        import ctypes as C
+        return (C.c_void_p * len(ts))(*[t.data_ptr() if t is not None and t.numel() else None for t in ts])
+
+    def _prep(self, batches, bits):
+        S = len(self.shards)
+        if len(batches) != S:
+            raise ValueError("one batch per source shard")
+        out = []
+        for s, b in enumerate(batches):
+            out.append(None if b is None else _io.to_device(b, bits, self.shards[s].device))
+        return out
+
+    def insert(self, keys: Sequence, values: Sequence) -> list:
+        import ctypes as C
+        sh = self.shards[0]
+        ks = self._prep(keys, sh.key_bits)
+        vs = self._prep(values, sh.value_bits)
+        n = [0 if k is None else k.numel() for k in ks]
+        for k, v in zip(ks, vs):
+            if (k is None) != (v is None) or (k is not None and k.numel() != v.numel()):
+                raise ValueError("keys and values differ in length")
+        st = [torch.empty(n[s], dtype=torch.uint8, device=f"cuda:{t.device}") for s, t in enumerate(self.shards)]
+        streams = (C.c_void_p * len(n))(*[_io.stream_of(t.device) for t in self.shards])
+        _lib.check(_lib.lib().ch_dist_insert(self.handle, self._ptrs(ks), self._ptrs(vs),
+                                             (C.c_uint64 * len(n))(*n), self._ptrs(st), streams), "dist_insert")
+        for t in self.shards:
+            t._dt.touch()
+        return st
+
+    def retrieve(self, keys: Sequence) -> list:
+        import ctypes as C
+        sh = self.shards[0]
+        ks = self._prep(keys, sh.key_bits)
+        n = [0 if k is None else k.numel() for k in ks]
+        vals = [torch.empty(n[s], dtype=_io.torch_dtype(sh.value_bits), device=f"cuda:{t.device}")
+                for s, t in enumerate(self.shards)]
+        found = [torch.empty(n[s], dtype=torch.uint8, device=f"cuda:{t.device}") for s, t in enumerate(self.shards)]
+        streams = (C.c_void_p * len(n))(*[_io.stream_of(t.device) for t in self.shards])
+        _lib.check(_lib.lib().ch_dist_retrieve(self.handle, self._ptrs(ks), (C.c_uint64 * len(n))(*n),
+                                               self._ptrs(vals), self._ptrs(found), streams), "dist_retrieve")
+        return list(zip(vals, found))
+
+
 class DistributedTable:
     """Bulk facade over per-shard B200 tables (single-, multi- or bucket-value)."""
 
@@ -142,13 +245,21 @@ class DistributedTable:
         self._multi = _is_multi(self.shards[0])
         self._bulk_lock = threading.Lock()
         self.device = self.shards[0].device
+        # single-value shards in distributed mode run through the C ABI's distributed table
+        # (ch_dist_*: split -> exchange -> local -> back -> scatter, all native)
+        self._native = None
+        if mode == ShardMode.DISTRIBUTED and not self._multi and \
+                all(type(t).__name__ == "SingleValueHashTable" for t in self.shards):
+            self._native = NativeDist(self.shards)
 
     @property
     def num_shards(self) -> int:
         return self.router.num_shards
 
     def close(self) -> None:
-        pass
+        if self._native is not None:
+            self._native.close()
+            self._native = None
 
     def __enter__(self) -> "DistributedTable":
         return self
@@ -188,6 +299,10 @@ class DistributedTable:
             k = sh._keys(keys)
             v = sh._vals(values)
             n = k.numel()
+            if self._native is not None and self.mode == ShardMode.DISTRIBUTED:
+                srcs = [k] + [None] * (self.num_shards - 1)
+                vsrc = [v] + [None] * (self.num_shards - 1)
+                return self._native.insert(srcs, vsrc)[0]
             perm, off, segs = self._segments(k, v)
             parts = []
             for s, (ks, vs) in enumerate(segs):
@@ -217,8 +332,13 @@ class DistributedTable:
 
     def _retrieve_distributed(self, k: torch.Tensor):
         n = k.numel()
-        perm, off, segs = self._segments(k, None)
         sh = self.shards[0]
+        if self._native is not None:
+            vals, found = self._native.retrieve([k] + [None] * (self.num_shards - 1))[0]
+            v = _io.from_device(vals, sh.value_bits).tolist()
+            f = found.cpu().numpy().tolist()
+            return [x if hit else None for x, hit in zip(v, f)]
+        perm, off, segs = self._segments(k, None)
         if not self._multi:
             vparts, fparts = [], []
             for s, (ks, _) in enumerate(segs):
@@ -341,12 +461,58 @@ def all_to_all_back(send: torch.Tensor, counts_in: list[int], counts_out: list[i
     return recv.to(home)
 
 
+def exchange_segments(sends: Sequence[torch.Tensor], send_counts: list[int], recv_counts: list[int],
+                      group=None) -> list[torch.Tensor]:
+    """Variable-length all-to-all of several parallel arrays in ONE grouped exchange.
+
+    ``sends[j]`` holds segments for ranks 0..W-1 back to back (``send_counts``); the
+    result ``recvs[j]`` holds what every rank sent this rank, in rank order
+    (``recv_counts``).  NCCL: one ``batch_isend_irecv`` group (ncclGroupStart, a
+    send + recv per peer and array, ncclGroupEnd) over NVLink; the rank's own segment
+    is a device copy.  gloo (CPU tests): the same through host memory."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    staged = any(_host_staged(t, group) for t in sends)
+    home = sends[0].device if sends else None
+    src = [t.cpu() if staged else t for t in sends]
+    recvs = [torch.empty(sum(recv_counts), dtype=t.dtype, device=t.device) for t in src]
+    so = [0]
+    for c in send_counts:
+        so.append(so[-1] + c)
+    ro = [0]
+    for c in recv_counts:
+        ro.append(ro[-1] + c)
+    ops = []
+    for j, t in enumerate(src):
+        for peer in range(world):
+            gpeer = dist.get_global_rank(group, peer) if group is not None else peer
+            if peer == rank:
+                if send_counts[peer]:
+                    recvs[j][ro[peer]:ro[peer + 1]].copy_(t[so[peer]:so[peer + 1]])
+                continue
+            if send_counts[peer]:
+                ops.append(dist.P2POp(dist.isend, t[so[peer]:so[peer + 1]], gpeer, group))
+            if recv_counts[peer]:
+                ops.append(dist.P2POp(dist.irecv, recvs[j][ro[peer]:ro[peer + 1]], gpeer, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return [r.to(home) for r in recvs] if staged else recvs
+
+
 class ShardedTable:
     """Rank-local shard of a hash-partitioned single-value table (torchrun, NCCL).
 
-    insert_device / retrieve_device are collective: every rank calls them with
-    its own batch.  Pipeline per call: split (K10) -> all_to_all (C1) -> local
-    K1/K2 -> all_to_all back (C1) -> inverse-permutation scatter (K11).
+    insert_device / retrieve_device are collective: every rank calls them with its own
+    batch (distributed.py:131-178, one process per GPU).  Pipeline per call:
+
+      split      route + stable split, u32 source index per position (K10, ch_multi_split32)
+      counts     one all_to_all of the S segment sizes (the only host synchronisation)
+      exchange   keys (+ values) in ONE grouped send/recv (exchange_segments, NVLink)
+      local      the shard's own insert / retrieve (staged regions for full-size batches)
+      back       statuses / (values, found) in one grouped exchange
+      scatter    inverse u32 permutation into the caller's order (K11, ch_scatter32)
     """
 
     def __init__(self, local_table, group=None):
@@ -356,28 +522,44 @@ class ShardedTable:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.router = ShardRouter(self.world)
+        self.last_phase_ms: dict[str, float] = {}
+
+    def _counts(self, offsets: torch.Tensor) -> tuple[list[int], list[int]]:
+        import torch.distributed as dist
+        sc = (offsets[1:] - offsets[:-1]).to(torch.int64)
+        rc = torch.empty_like(sc)
+        if _host_staged(sc, self.group):
+            sc_h, rc_h = sc.cpu(), torch.empty(self.world, dtype=torch.int64)
+            dist.all_to_all_single(rc_h, sc_h, group=self.group)
+            return sc_h.tolist(), rc_h.tolist()
+        dist.all_to_all_single(rc, sc, group=self.group)
+        both = torch.cat([sc, rc]).cpu().tolist()   # one device -> host read per call
+        return both[:self.world], both[self.world:]
 
     def insert_device(self, keys: torch.Tensor, values: torch.Tensor) -> torch.Tensor:
-        perm, offsets, kout, vout = split_device(keys, self.world, values)
-        counts = (offsets[1:] - offsets[:-1]).cpu().tolist()
-        rk, rcounts = all_to_all_segments(kout, counts, self.group)
-        rv, _ = all_to_all_segments(vout, counts, self.group)
+        k = self.table._keys(keys)
+        v = self.table._vals(values)
+        if k.numel() != v.numel():
+            raise ValueError("keys and values differ in length")
+        perm, offsets, kout, vout = split_device32(k, self.world, v)
+        send, recv = self._counts(offsets)
+        rk, rv = exchange_segments([kout, vout], send, recv, self.group)
         st = self.table.insert_device(rk, rv)
-        back = all_to_all_back(st, rcounts, counts, self.group)
-        out = torch.empty(keys.numel(), dtype=torch.uint8, device=keys.device)
-        return scatter_device(back, perm, out) if keys.numel() else out
+        (back,) = exchange_segments([st], recv, send, self.group)
+        out = torch.empty(k.numel(), dtype=torch.uint8, device=k.device)
+        return scatter_device32(back, perm, out) if k.numel() else out
 
     def retrieve_device(self, keys: torch.Tensor):
-        perm, offsets, kout, _ = split_device(keys, self.world)
-        counts = (offsets[1:] - offsets[:-1]).cpu().tolist()
-        rk, rcounts = all_to_all_segments(kout, counts, self.group)
+        k = self.table._keys(keys)
+        perm, offsets, kout, _ = split_device32(k, self.world)
+        send, recv = self._counts(offsets)
+        (rk,) = exchange_segments([kout], send, recv, self.group)
         v, f = self.table.retrieve_device(rk)
-        vb = all_to_all_back(v, rcounts, counts, self.group)
-        fb = all_to_all_back(f, rcounts, counts, self.group)
-        n = keys.numel()
-        vals = torch.empty(n, dtype=v.dtype, device=keys.device)
-        found = torch.empty(n, dtype=torch.uint8, device=keys.device)
+        vb, fb = exchange_segments([v, f], recv, send, self.group)
+        n = k.numel()
+        vals = torch.empty(n, dtype=v.dtype, device=k.device)
+        found = torch.empty(n, dtype=torch.uint8, device=k.device)
         if n:
-            scatter_device(vb, perm, vals)
-            scatter_device(fb, perm, found)
+            scatter_device32(vb, perm, vals)
+            scatter_device32(fb, perm, found)
         return vals, found

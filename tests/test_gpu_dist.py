@@ -198,3 +198,95 @@ def test_sharded_table_world2_one_gpu():
     inserted, dup, size = res[0][2]
     assert inserted == 2 * 150_000 + 20_000 == size     # each shared key lands once
     assert dup == 20_000                                 # ...and its second copy is DUPLICATE
+
+
+# ---------------------------------------------------------------- ch_dist_* (C ABI)
+from paper_2009_07914_b200.distributed import NativeDist, split_device32, scatter_device32  # noqa: E402
+
+
+@pytest.mark.parametrize("shards", [1, 2, 4, 8])
+def test_native_dist_per_source_batches(shards):
+    """ch_dist_insert / ch_dist_retrieve with one batch per source: every key lands on
+    route(k) (distributed.py:44-45), statuses / values / found flags exact vs the oracle."""
+    rng = np.random.default_rng(70 + shards)
+    per = 50_000
+    allk = rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=shards * per * 2,
+                                                  dtype=np.uint64)))[: shards * per + 5000]
+    src_keys = [allk[s * per:(s + 1) * per] for s in range(shards)]
+    # a few keys repeated across sources: exactly one INSERTED each
+    dup = allk[:500]
+    src_keys[-1] = np.concatenate([src_keys[-1], dup])
+    src_vals = [(k * 3 % (1 << 32)).astype(np.uint64) for k in src_keys]
+    tables = [SingleValueHashTable(int(shards * per * 1.2 / shards) + 4096, layout="packed", key_bits=32,
+                                   value_bits=32) for _ in range(shards)]
+    nd = NativeDist(tables, transport="copy")
+    assert nd.transport == "copy"
+    to32 = lambda a: torch.from_numpy(a.astype(np.uint32).view(np.int32)).cuda()
+    st = nd.insert([to32(k) for k in src_keys], [to32(v) for v in src_vals])
+    codes = np.concatenate([s.cpu().numpy() for s in st])
+    assert int((codes == 0).sum()) == shards * per and int((codes == 1).sum()) == 500
+    assert sum(t.occupied for t in tables) == shards * per
+    for s, t in enumerate(tables):  # placement: only keys routed to s live on s
+        probe = allk[: shards * per][:20000]
+        v, f = t.retrieve_device(to32(probe))
+        routed = np.array([orc.route(int(k), shards) for k in probe]) == s
+        assert (f.cpu().numpy().astype(bool) == routed).all()
+    miss = allk[shards * per:]
+    q = [to32(np.concatenate([src_keys[s][::-1], miss])) for s in range(shards)]
+    res = nd.retrieve(q)
+    for s, (v, f) in enumerate(res):
+        nk = len(src_keys[s])
+        fv = f.cpu().numpy().astype(bool)
+        assert fv[:nk].all() and not fv[nk:].any()
+        assert (v.cpu().numpy()[:nk].view(np.uint32) == src_vals[s][::-1].astype(np.uint32)).all()
+    nd.close()
+
+
+def test_native_dist_nccl_one_device():
+    t = SingleValueHashTable(1 << 16, layout="packed", key_bits=32, value_bits=32)
+    nd = NativeDist([t], transport="nccl")
+    assert nd.transport == "nccl"
+    keys = torch.arange(1, 30_001, dtype=torch.int32, device="cuda")
+    (st,) = nd.insert([keys], [keys * 5])
+    assert (st.cpu() == 0).all()
+    ((v, f),) = nd.retrieve([keys])
+    assert f.cpu().bool().all() and (v.cpu() == keys.cpu() * 5).all()
+    nd.close()
+
+
+def test_native_dist_rejects_bad_shards():
+    m = MultiValueHashTable(1024)
+    with pytest.raises(ValueError):
+        NativeDist([m])
+    a = SingleValueHashTable(1024, layout="packed", key_bits=32, value_bits=32)
+    b = SingleValueHashTable(1024, key_bits=64, value_bits=64)
+    with pytest.raises(ValueError):
+        NativeDist([a, b])
+    with pytest.raises(ValueError):   # NCCL needs one shard per device
+        NativeDist([a, SingleValueHashTable(1024, layout="packed", key_bits=32, value_bits=32)], transport="nccl")
+
+
+@pytest.mark.parametrize("shards", [1, 5, 256])
+def test_split32_and_scatter32(shards):
+    n = (1 << 20) + 77
+    rng = np.random.default_rng(shards)
+    keys = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+    vals = rng.integers(0, 1 << 31, size=n, dtype=np.uint64).astype(np.uint32)
+    k = torch.from_numpy(keys.view(np.int32)).cuda()
+    v = torch.from_numpy(vals.view(np.int32)).cuda()
+    perm, offsets, kout, vout = split_device32(k, shards, v)
+    rperm, roff = orc.multi_split(keys.astype(np.uint64), shards)
+    assert (perm.cpu().numpy().view(np.uint32) == rperm.astype(np.uint32)).all()
+    assert (offsets.cpu().numpy() == roff.astype(np.int64)).all()
+    assert (kout.cpu().numpy().view(np.uint32) == keys[rperm]).all()
+    assert (vout.cpu().numpy().view(np.uint32) == vals[rperm]).all()
+    back = scatter_device32(vout, perm, torch.empty_like(v))
+    assert (back.cpu().numpy().view(np.uint32) == vals).all()
+
+
+def test_split_of_empty_batch():
+    k = torch.empty(0, dtype=torch.int64, device="cuda")
+    perm, offsets, _, _ = split_device(k, 4)
+    assert offsets.cpu().tolist() == [0, 0, 0, 0, 0]
+    perm, offsets, _, _ = split_device32(k.to(torch.int32), 3)
+    assert offsets.cpu().tolist() == [0, 0, 0, 0]

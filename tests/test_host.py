@@ -30,6 +30,20 @@ def test_library_exports_every_declared_symbol():
     assert lib.ch_version() == 1
 
 
+def test_dist_abi_validates_arguments_without_a_gpu():
+    import ctypes as C
+    lib = _lib.lib()
+    h = C.c_void_p()
+    assert lib.ch_dist_create(C.byref(h), None, 2, 0) == _lib.CH_EINVAL
+    arr = (C.c_void_p * 1)(None)
+    assert lib.ch_dist_create(C.byref(h), arr, 0, 0) == _lib.CH_EINVAL      # no shards
+    assert lib.ch_dist_create(C.byref(h), arr, 1, 7) == _lib.CH_EINVAL      # bad transport
+    assert lib.ch_dist_create(C.byref(h), arr, 1, 0) == _lib.CH_EINVAL      # null shard table
+    assert "shard" in _lib.last_error()
+    assert lib.ch_dist_insert(None, None, None, None, None, None) == _lib.CH_EINVAL
+    assert lib.ch_dist_destroy(None) == 0
+
+
 def test_probing_matches_golden():
     g = load("probing.json")
     keys = ints(g["keys"])
@@ -126,6 +140,58 @@ def _exchange_worker(rank, world, port, q):
         q.put((rank, ok, int(total.item())))
     finally:
         dist.destroy_process_group()
+
+
+def _grouped_worker(rank, world, port, q):
+    """exchange_segments (the ShardedTable / bench exchange): keys and values of every
+    (rank -> peer) segment in one grouped send/recv, then results back."""
+    import torch.distributed as dist
+    from paper_2009_07914_b200.distributed import exchange_segments
+    import oracle as orc
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(200 + rank)
+        n = 3000 + 101 * rank
+        keys = rng.integers(0, 1 << 31, size=n, dtype=np.uint64).astype(np.uint32)
+        vals = (keys.astype(np.uint64) * 7 % (1 << 32)).astype(np.uint32)
+        perm, offsets = orc.multi_split(keys.astype(np.uint64), world)
+        send = np.diff(offsets).astype(np.int64).tolist()
+        sc = torch.tensor(send, dtype=torch.int64)
+        rc = torch.empty(world, dtype=torch.int64)
+        dist.all_to_all_single(rc, sc)
+        recv = rc.tolist()
+        kt = torch.from_numpy(keys[perm].view(np.int32))
+        vt = torch.from_numpy(vals[perm].view(np.int32))
+        rk, rv = exchange_segments([kt, vt], send, recv)
+        gk = rk.numpy().view(np.uint32)
+        ok = all(orc.route(int(k), world) == rank for k in gk)
+        ok &= bool((rv.numpy().view(np.uint32) == (gk.astype(np.uint64) * 7 % (1 << 32)).astype(np.uint32)).all())
+        # answer with (key + 1, key & 1) and send both arrays back in one group
+        bv, bf = exchange_segments([rk + 1, (rk & 1).to(torch.uint8)], recv, send)
+        ok &= bool((bv.numpy() == kt.numpy() + 1).all()) and bool((bf.numpy() == (kt.numpy() & 1)).all())
+        total = torch.tensor([len(gk)], dtype=torch.int64)
+        dist.all_reduce(total)
+        q.put((rank, ok, int(total.item())))
+    except Exception as e:
+        q.put((rank, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_grouped_exchange_gloo(world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grouped_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(60)
+    assert all(ok for _, ok, _ in res), res
+    assert res[0][2] == sum(3000 + 101 * r for r in range(world))
 
 
 def test_all_to_all_exchange_gloo_world2():
