@@ -150,6 +150,8 @@ int ch_bucket_retrieve(ch_table* t, const uint64_t* d_handles, uint64_t n,
 /* copy the slot arrays to host: keys[c] and values[c] in storage widths
  * (packed tables return key / value halves split) */
 int ch_read_slots(ch_table* t, void* h_keys, void* h_vals);
+/* cells [start, start + count) only (single-cell reads of the SlotArray view) */
+int ch_read_slot_range(ch_table* t, uint64_t start, uint64_t count, void* h_keys, void* h_vals);
 int ch_write_slots(ch_table* t, const void* h_keys, const void* h_vals); /* test fixtures */
 int ch_read_arena(ch_table* t, void* h_arena, uint64_t count);
 /* element transitions on one slot (layout.py:140-243), for SlotArray parity:

@@ -69,6 +69,7 @@ _SIGS = {
     "ch_bucket_retrieve": (C.c_int, [_P, _P, _U64, _P, _P, _P]),
     "ch_read_slots": (C.c_int, [_P, _P, _P]),
     "ch_write_slots": (C.c_int, [_P, _P, _P]),
+    "ch_read_slot_range": (C.c_int, [_P, _U64, _U64, _P, _P]),
     "ch_read_arena": (C.c_int, [_P, _P, _U64]),
     "ch_slot_op": (C.c_int, [_P, C.c_int, _U64, _U64, _U64, _U64, C.POINTER(C.c_int),
                              C.POINTER(_U64), C.POINTER(_U64)]),

@@ -308,6 +308,7 @@ class BucketListHashTable(_TableBase):
         if not keys:
             return [0], []
         offsets, vals = self.retrieve_device(keys)
+        self._dt.stats()  # raises ContentionTimeout if a walk met a handle left BLOCKED (:300-318)
         return offsets.cpu().numpy().tolist(), _io.from_device(vals, self.value_bits).tolist()
 
     def for_each(self, keys: Iterable[int], callback: Callable[[int, int, int], None]) -> None:

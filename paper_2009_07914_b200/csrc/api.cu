@@ -692,35 +692,45 @@ int ch_bucket_retrieve(ch_table* t, const uint64_t* handles, uint64_t n, const u
   return o.done(bucket_walk(o.lc, bucket_ref(t), t->vbytes, handles, n, offsets, vals_out));
 }
 
-int ch_read_slots(ch_table* t, void* h_keys, void* h_vals) {
+int ch_read_slot_range(ch_table* t, uint64_t start, uint64_t count, void* h_keys, void* h_vals) {
   if (!t) return fail(CH_EINVAL, "null table");
+  if (start > t->T.c || count > t->T.c - start) return fail(CH_EINVAL, "slot range out of bounds");
   std::lock_guard<std::mutex> lock(t->mu);
   DeviceGuard dev(t->cfg.device);
   int rc = check(cudaEventSynchronize(t->last), "synchronize");
-  if (rc) return rc;
-  const uint64_t c = t->T.c;
+  if (rc || count == 0) return rc;
   const int kb = t->ts.kbytes, vb = t->ts.vbytes;
   if (t->cfg.layout == CH_SOA) {
-    if (h_keys) rc = check(cudaMemcpy(h_keys, t->T.slots, c * kb, cudaMemcpyDeviceToHost), "read keys");
-    if (!rc && h_vals) rc = check(cudaMemcpy(h_vals, t->T.vals, c * vb, cudaMemcpyDeviceToHost), "read values");
+    if (h_keys)
+      rc = check(cudaMemcpy(h_keys, (const char*)t->T.slots + start * kb, count * kb, cudaMemcpyDeviceToHost),
+                 "read keys");
+    if (!rc && h_vals)
+      rc = check(cudaMemcpy(h_vals, (const char*)t->T.vals + start * vb, count * vb, cudaMemcpyDeviceToHost),
+                 "read values");
     return rc;
   }
   const size_t cell = t->cfg.layout == CH_PACKED ? 8 : (kb == 8 || vb == 8 ? 16 : 8);
   std::vector<unsigned char> buf;
   try {
-    buf.resize(c * cell);
+    buf.resize(count * cell);
   } catch (...) {
     return fail(CH_ENOMEM, "host buffer");
   }
-  rc = check(cudaMemcpy(buf.data(), t->T.slots, c * cell, cudaMemcpyDeviceToHost), "read cells");
+  rc = check(cudaMemcpy(buf.data(), (const char*)t->T.slots + start * cell, count * cell, cudaMemcpyDeviceToHost),
+             "read cells");
   if (rc) return rc;
   const size_t voff = t->cfg.layout == CH_PACKED ? 4 : (cell == 16 ? 8 : 4);
-  for (uint64_t i = 0; i < c; ++i) {
+  for (uint64_t i = 0; i < count; ++i) {
     const unsigned char* p = buf.data() + i * cell;
     if (h_keys) memcpy((char*)h_keys + i * kb, p, kb);
     if (h_vals) memcpy((char*)h_vals + i * vb, p + voff, vb);
   }
   return CH_OK;
+}
+
+int ch_read_slots(ch_table* t, void* h_keys, void* h_vals) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  return ch_read_slot_range(t, 0, t->T.c, h_keys, h_vals);
 }
 
 int ch_write_slots(ch_table* t, const void* h_keys, const void* h_vals) {

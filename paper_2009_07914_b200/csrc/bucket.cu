@@ -249,17 +249,29 @@ __global__ void k_bucket_walk(BucketRef B, const uint64_t* __restrict__ handles,
     const uint64_t want = offsets[i + 1] - offsets[i];
     if (!want) continue;
     const uint64_t h = handles[i];
+    if ((h >> 62) == 1) {
+      // BLOCKED (bucket_list.py:300-318): batches are stream-ordered, so no insert of this
+      // library is ever in flight here -- the handle was left blocked from outside and
+      // would never become ready.  The reference raises ContentionTimeout after its retry
+      // budget; the sticky device error bit 0 makes the host raise the same.
+      atomicOr(&B.T.ctr->error, 1ull);
+      continue;
+    }
     const uint64_t count = (h >> TAIL_BITS) & COUNT_MAX;
     const uint64_t take_all = count < want ? count : want;  // raced writer: keep the segment length
     uint64_t base = h & TAIL_MAX;
     const uint64_t m = B.gr.buckets_for(count);
     for (uint64_t bb = m; bb-- > 0;) {
+      if (base >= B.pool_cap) {  // a chain reference outside the arena: corrupt handle / header
+        atomicOr(&B.T.ctr->error, 2ull);
+        break;
+      }
       const uint64_t first = B.gr.before(bb);
       if (first < take_all) {
         const uint64_t sz = B.gr.size(bb);
         const uint64_t take = (take_all - first) < sz ? (take_all - first) : sz;
         const uint64_t src = base + (bb > 0 ? 1 : 0);
-        for (uint64_t k = 0; k < take; ++k) out[offsets[i] + first + k] = arena[src + k];
+        for (uint64_t k = 0; k < take && src + k < B.pool_cap; ++k) out[offsets[i] + first + k] = arena[src + k];
       }
       if (bb > 0) base = (uint64_t)arena[base];
     }

@@ -124,9 +124,12 @@ class DeviceTable:
     def stats(self) -> _lib.ch_stats:
         s = _lib.ch_stats()
         _lib.check(_lib.lib().ch_get_stats(self.handle, C.byref(s)), "ch_get_stats")
-        if s.device_error:
+        if s.device_error & 1:
             from .bucket_list import ContentionTimeout
             raise ContentionTimeout("a bucket handle stayed blocked past the retry budget")
+        if s.device_error:
+            raise RuntimeError(f"device error bits {s.device_error:#x}: a list handle or bucket header "
+                               "points outside the arena")
         return s
 
     def read_slots(self, value_bits: int | None = None) -> tuple[np.ndarray, np.ndarray]:
@@ -136,6 +139,16 @@ class DeviceTable:
         vals = np.empty(self.capacity, dtype=vd)
         _lib.check(_lib.lib().ch_read_slots(self.handle, keys.ctypes.data, vals.ctypes.data),
                    "ch_read_slots")
+        return keys, vals
+
+    def read_range(self, start: int, count: int, value_bits: int | None = None) -> tuple[np.ndarray, np.ndarray]:
+        """Cells [start, start + count) only (no whole-table copy)."""
+        kd = storage_dtype(self.key_bits)
+        vd = storage_dtype(self.value_bits if value_bits is None else value_bits)
+        keys = np.empty(count, dtype=kd)
+        vals = np.empty(count, dtype=vd)
+        _lib.check(_lib.lib().ch_read_slot_range(self.handle, start, count, keys.ctypes.data, vals.ctypes.data),
+                   "ch_read_slot_range")
         return keys, vals
 
     def slot_op(self, op: int, slot: int, expected: int = 0, desired: int = 0,
@@ -191,24 +204,42 @@ class SlotArray:
                 self._cache_version = v
             return self._keys, self._vals
 
+    def _cells(self, start: int, count: int) -> tuple[np.ndarray, np.ndarray]:
+        """Cells [start, start + count) (count <= capacity, wrapping): served from the
+        whole-array host copy when it is current, else read from the device alone --
+        element reads of a 2 GiB table move bytes, not the table."""
+        with self._lock:
+            cached = self._cache_version == self._t.version
+        if cached:
+            idx = (np.arange(count, dtype=np.int64) + start) % self.capacity
+            return self._keys[idx], self._vals[idx]
+        first = min(count, self.capacity - start)
+        k, v = self._t.read_range(start, first, self.value_bits)
+        if first < count:
+            k2, v2 = self._t.read_range(0, count - first, self.value_bits)
+            k, v = np.concatenate([k, k2]), np.concatenate([v, v2])
+        return k, v
+
+    def _index(self, i: int) -> int:
+        if not -self.capacity <= i < self.capacity:
+            raise IndexError("slot index out of range")
+        return i % self.capacity
+
     def load_window(self, start: int, width: int) -> list[int]:
-        keys, _ = self._host()
-        c = self.capacity
-        idx = (np.arange(width, dtype=np.int64) + start % c) % c
-        return keys[idx].tolist()
+        return self._cells(start % self.capacity, width)[0].tolist()
 
     def load_key(self, i: int) -> int:
-        return int(self._host()[0][i])
+        return int(self._cells(self._index(i), 1)[0][0])
 
     def load_value(self, i: int) -> int:
-        return int(self._host()[1][i])
+        return int(self._cells(self._index(i), 1)[1][0])
 
     def load_pair(self, i: int) -> tuple[int, int]:
         if self.layout == LayoutKind.PACKED_AOS:  # one atomic 64-bit read (layout.py:154-157)
             _, k, v = self._t.slot_op(5, i)
             return k, v
-        keys, vals = self._host()
-        return int(keys[i]), int(vals[i])
+        k, v = self._cells(self._index(i), 1)
+        return int(k[0]), int(v[0])
 
     def store_value(self, i: int, value: int) -> None:
         self._t.slot_op(4, i, value=value)

@@ -170,3 +170,17 @@ def test_exact_policy_maximizes_density():   # test_bucket_list.py:306-319
         t.insert_bulk([(k, i) for k in keys for i in range(r)])
         dens[name] = t.storage_density()
     assert dens["exact"] == max(dens.values())
+
+
+def test_blocked_handle_raises_contention_timeout():
+    """A handle left BLOCKED (bucket_list.py:300-318) never becomes ready; the walk flags it
+    and the list API raises ContentionTimeout, like the reference after its retry budget."""
+    from paper_2009_07914_b200 import ContentionTimeout, pack_handle
+    t = BucketListHashTable(64, 256, key_bits=32, value_bits=32)
+    t.insert_bulk([(5, 50), (5, 51), (9, 90)])
+    assert sorted(t.retrieve(5)) == [50, 51]
+    slot = t.key_store.slot_of(5)
+    t.slots.store_value(slot, pack_handle(1, 2, 0))   # BLOCKED, count 2
+    assert t.retrieve(9) == [90]                        # other keys are unaffected
+    with pytest.raises(ContentionTimeout):
+        t.retrieve_bulk([5, 9])
