@@ -330,14 +330,37 @@ class DistributedTable:
                 return self._retrieve_distributed(k)
             return self._retrieve_independent(k)
 
-    def _retrieve_distributed(self, k: torch.Tensor):
-        n = k.numel()
+    def retrieve_device(self, keys):
+        """Bulk retrieval over CUDA tensors: (values, found) for single-value shards,
+        (offsets int64[n+1], flat values) for multi-value / bucket shards, on the
+        device of shard 0 (distributed.py:151-203)."""
+        with self._bulk_lock:
+            k = self.shards[0]._keys(keys)
+            if self.mode == ShardMode.DISTRIBUTED:
+                return self._retrieve_distributed_device(k)
+            return self._retrieve_independent_device(k)
+
+    def _to_lists(self, res):
         sh = self.shards[0]
-        if self._native is not None:
-            vals, found = self._native.retrieve([k] + [None] * (self.num_shards - 1))[0]
+        if not self._multi:
+            vals, found = res
             v = _io.from_device(vals, sh.value_bits).tolist()
             f = found.cpu().numpy().tolist()
             return [x if hit else None for x, hit in zip(v, f)]
+        offsets, flat = res
+        return offsets.cpu().tolist(), _io.from_device(flat, sh.value_bits).tolist()
+
+    def _retrieve_distributed(self, k: torch.Tensor):
+        return self._to_lists(self._retrieve_distributed_device(k))
+
+    def _retrieve_independent(self, k: torch.Tensor):
+        return self._to_lists(self._retrieve_independent_device(k))
+
+    def _retrieve_distributed_device(self, k: torch.Tensor):
+        n = k.numel()
+        sh = self.shards[0]
+        if self._native is not None:
+            return self._native.retrieve([k] + [None] * (self.num_shards - 1))[0]
         perm, off, segs = self._segments(k, None)
         if not self._multi:
             vparts, fparts = [], []
@@ -347,9 +370,7 @@ class DistributedTable:
                 fparts.append(self._to_shard(f, 0))
             vals = scatter_device(torch.cat(vparts), perm, sh._empty_vals(n))
             found = scatter_device(torch.cat(fparts), perm, sh._u8(n))
-            v = _io.from_device(vals, sh.value_bits).tolist()
-            f = found.cpu().numpy().tolist()
-            return [x if hit else None for x, hit in zip(v, f)]
+            return vals, found
         # multi-value: per-shard (offsets, flat) -> global offsets in query order -> segmented copy
         cparts, oparts, fparts = [], [], []
         base = 0
@@ -369,11 +390,11 @@ class DistributedTable:
             _lib.check(_lib.lib().ch_segment_copy(flat_src.data_ptr(), flat_src.element_size(), src_off.data_ptr(),
                                                   perm.data_ptr(), n, dst_off.data_ptr(), flat.data_ptr(),
                                                   k.device.index, _io.stream_of(k.device.index)), "segment copy")
-        return dst_off.cpu().tolist(), _io.from_device(flat, sh.value_bits).tolist()
+        return dst_off, flat
 
-    def _retrieve_independent(self, k: torch.Tensor):
-        # broadcast the queries; lowest shard id wins for single-value, concatenation for
-        # multi-value (distributed.py:180-195)
+    def _retrieve_independent_device(self, k: torch.Tensor):
+        # broadcast the queries; lowest shard id wins for single-value, concatenation in shard
+        # order for multi-value (distributed.py:180-195)
         n = k.numel()
         sh = self.shards[0]
         if not self._multi:
@@ -385,18 +406,20 @@ class DistributedTable:
                 take = f & ~found
                 vals = torch.where(take, v, vals)
                 found |= f
-            v = _io.from_device(vals, sh.value_bits).tolist()
-            f = found.cpu().numpy().tolist()
-            return [x if hit else None for x, hit in zip(v, f)]
-        per_key: list[list[int]] = [[] for _ in range(n)]
-        for s in range(self.num_shards):
-            o, f = self.shards[s].retrieve_device(self._to_shard(k, s))
-            o = o.cpu().tolist()
-            f = _io.from_device(f, sh.value_bits).tolist()
-            for i in range(n):
-                per_key[i].extend(f[o[i]:o[i + 1]])
-        offsets = exclusive_prefix_sum([len(p) for p in per_key])
-        return offsets, [v for p in per_key for v in p]
+            return vals, found.to(torch.uint8)
+        res = [self.shards[s].retrieve_device(self._to_shard(k, s)) for s in range(self.num_shards)]
+        res = [(self._to_shard(o, 0), self._to_shard(f, 0)) for o, f in res]
+        counts = [(o[1:] - o[:-1]) for o, _ in res]
+        total_counts = torch.stack(counts).sum(0) if counts else torch.zeros(n, dtype=torch.int64, device=k.device)
+        offsets = exclusive_prefix_sum(total_counts.to(torch.int32))
+        flat = torch.zeros(int(offsets[n].item()), dtype=res[0][1].dtype, device=k.device)
+        base = offsets[:-1].clone()
+        for (o, f), c in zip(res, counts):   # shard s's segment of query i follows shards < s
+            if f.numel():
+                seg_start = torch.repeat_interleave(base - o[:-1], c)
+                flat[seg_start + torch.arange(f.numel(), device=k.device)] = f
+            base += c
+        return offsets, flat
 
     def count_bulk(self, keys: Sequence[int]) -> list[int]:
         if not self._multi:
