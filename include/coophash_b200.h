@@ -135,6 +135,21 @@ int ch_multi_count(ch_table* t, const void* d_keys, uint64_t n, uint32_t* d_coun
 int ch_multi_retrieve(ch_table* t, const void* d_keys, uint64_t n, const uint64_t* d_offsets,
                       void* d_vals_out, void* stream);
 
+/* for_each on a multi-value table (multi_table.py:299-328): ch_multi_retrieve plus the slot
+ * index of every value (d_slots_out at the same positions) */
+int ch_multi_retrieve_slots(ch_table* t, const void* d_keys, uint64_t n, const uint64_t* d_offsets,
+                            void* d_vals_out, int64_t* d_slots_out, void* stream);
+
+/* ---- device functors: for_all (single_table.py:425-429, multi_table.py:330-339) ----
+ * the live cells (neither empty nor tombstone) in slot order, compacted on the device:
+ * keys / values (storage widths; bucket tables: the list handles) / slot indices, any of
+ * them NULL; at most cap written; *d_count (device u64, may be NULL) = live cells */
+int ch_for_all(ch_table* t, void* d_keys_out, void* d_vals_out, int64_t* d_slots_out, uint64_t cap,
+               uint64_t* d_count, void* stream);
+/* built-in reductions over the live cells, one pass: d_out[5] = count, sum of values
+ * (mod 2^64), xor of keys, min value, max value (min = 2^64-1 when empty) */
+int ch_reduce_live(ch_table* t, uint64_t* d_out, void* stream);
+
 /* ---- bucket list (bucket_list.py) ---- */
 int ch_bucket_insert(ch_table* t, const void* d_keys, const void* d_vals, uint64_t n,
                      uint8_t* d_status, void* stream);             /* :228-294, :367-378 */

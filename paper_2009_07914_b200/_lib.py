@@ -64,6 +64,9 @@ _SIGS = {
     "ch_multi_insert": (C.c_int, [_P, _P, _P, _U64, _P, _P]),
     "ch_multi_count": (C.c_int, [_P, _P, _U64, _P, _P, _P]),
     "ch_multi_retrieve": (C.c_int, [_P, _P, _U64, _P, _P, _P]),
+    "ch_multi_retrieve_slots": (C.c_int, [_P, _P, _U64, _P, _P, _P, _P]),
+    "ch_for_all": (C.c_int, [_P, _P, _P, _P, _U64, _P, _P]),
+    "ch_reduce_live": (C.c_int, [_P, _P, _P]),
     "ch_bucket_insert": (C.c_int, [_P, _P, _P, _U64, _P, _P]),
     "ch_bucket_count": (C.c_int, [_P, _P, _U64, _P, _P, _P, _P]),
     "ch_bucket_retrieve": (C.c_int, [_P, _P, _U64, _P, _P, _P]),

@@ -10,6 +10,7 @@ the answers against an in-memory oracle and writes one CSV row per (point, opera
 wrong answer aborts with exit code 2 and no CSV.
 
 B200 differences, all additive:
+  * ``--warmup`` (default 1) untimed repetitions before the timed ones;
   * timing: CUDA events around the device bulk op with the inputs already in HBM (the
     reference times its Python call with the inputs materialised in host memory; the
     host -> device copy happens once, before the clock, like its list construction);
@@ -192,7 +193,8 @@ def _bucket_retrieve_bytes(counts: np.ndarray) -> float:
 # ------------------------------------------------------------------ sweeps
 
 def run_single_sweep(densities: Sequence[float], spec: WorkloadSpec, *, layout: str = "soa",
-                     group_width: int = 32, threads: int = 1, repeats: int = 10) -> list[BenchRecord]:
+                     group_width: int = 32, threads: int = 1, repeats: int = 10,
+                     warmup: int = 1) -> list[BenchRecord]:
     keys = gen_unique(spec)
     values = np.arange(1, spec.n + 1, dtype=np.uint64)
     vbits = 32 if layout == "packed" else 64
@@ -201,21 +203,21 @@ def run_single_sweep(densities: Sequence[float], spec: WorkloadSpec, *, layout: 
     for rho in sorted(densities):
         ins_secs = ret_secs = ins_att = ret_att = 0.0
         achieved = 0.0
-        for _ in range(repeats):
+        for rep in range(repeats + warmup):
             table = SingleValueHashTable(int(np.ceil(spec.n / rho)), layout=layout, key_bits=spec.key_bits,
                                          value_bits=vbits, group_width=group_width, workers=threads)
             c0 = table.probe_counters()
             secs, st = _timed(lambda: table.insert_device(dk, dv))
             _check_inserted(st, f"single-sweep rho={rho}")
-            ins_secs += secs
-            ins_att += _mean_attempts(table, c0)
+            ins_secs += secs if rep >= warmup else 0.0
+            ins_att += _mean_attempts(table, c0) if rep >= warmup else 0.0
             achieved = table.load_factor()
             c0 = table.probe_counters()
             secs, (got, found) = _timed(lambda: table.retrieve_device(dk))
             if not (bool(found.bool().all()) and np.array_equal(_host_u64(got), values)):
                 raise VerificationError(f"single-sweep rho={rho}: retrieval mismatch")
-            ret_secs += secs
-            ret_att += _mean_attempts(table, c0)
+            ret_secs += secs if rep >= warmup else 0.0
+            ret_att += _mean_attempts(table, c0) if rep >= warmup else 0.0
             del table
         for op, secs, att, b in (("insert", ins_secs, ins_att, INSERT_BYTES), ("retrieve", ret_secs, ret_att,
                                                                               RETRIEVE_BYTES)):
@@ -226,7 +228,8 @@ def run_single_sweep(densities: Sequence[float], spec: WorkloadSpec, *, layout: 
 
 
 def run_multi_sweep(multiplicities: Sequence[int], spec: WorkloadSpec, *, layout: str = "soa",
-                    group_width: int = 32, threads: int = 1, repeats: int = 10) -> list[BenchRecord]:
+                    group_width: int = 32, threads: int = 1, repeats: int = 10,
+                     warmup: int = 1) -> list[BenchRecord]:
     records: list[BenchRecord] = []
     vbits = 32 if layout == "packed" else 64
     for r in multiplicities:
@@ -241,22 +244,23 @@ def run_multi_sweep(multiplicities: Sequence[int], spec: WorkloadSpec, *, layout
         ins_secs = ret_secs = ins_att = ret_att = 0.0
         achieved = 0.0
         rbytes = 0.0
-        for _ in range(repeats):
+        for rep in range(repeats + warmup):
             table = MultiValueHashTable(int(np.ceil(wspec.n / rho)), layout=layout, key_bits=spec.key_bits,
                                         value_bits=vbits, group_width=group_width, workers=threads)
             c0 = table.probe_counters()
             secs, st = _timed(lambda: table.insert_device(dk, dv))
             _check_inserted(st, f"multi-sweep r={r}")
-            ins_secs += secs
-            ins_att += _mean_attempts(table, c0)
+            ins_secs += secs if rep >= warmup else 0.0
+            ins_att += _mean_attempts(table, c0) if rep >= warmup else 0.0
             achieved = table.load_factor()
             c0 = table.probe_counters()
             secs, (off, flat) = _timed(lambda: table.retrieve_device(dq))
             offsets = off.cpu().numpy()
             _verify_multi(queries, offsets, _host_u64(flat), ref, f"multi-sweep r={r}")
             rbytes = _multi_retrieve_bytes(np.diff(offsets))
-            ret_secs += secs
-            ret_att += _mean_attempts(table, c0)
+            del off, flat  # the next repetition's outputs reuse the cached blocks
+            ret_secs += secs if rep >= warmup else 0.0
+            ret_att += _mean_attempts(table, c0) if rep >= warmup else 0.0
             del table
         for op, secs, att, b in (("insert", ins_secs, ins_att, INSERT_BYTES * wspec.n),
                                  ("retrieve", ret_secs, ret_att, rbytes)):
@@ -277,7 +281,7 @@ def _parse_policy(name: str, r: int) -> tuple[str, GrowthPolicy]:
 
 
 def run_bucket_sweep(policies: Sequence[str], spec: WorkloadSpec, *, group_width: int = 32,
-                     threads: int = 1, repeats: int = 10) -> list[BenchRecord]:
+                     threads: int = 1, repeats: int = 10, warmup: int = 1) -> list[BenchRecord]:
     keys = gen_multiplicity(spec)
     vals = np.arange(1, spec.n + 1, dtype=np.uint64)
     queries = np.arange(1, spec.n + 1, dtype=np.uint64)
@@ -292,19 +296,20 @@ def run_bucket_sweep(policies: Sequence[str], spec: WorkloadSpec, *, group_width
         ins_secs = ret_secs = 0.0
         achieved = 0.0
         rbytes = 0.0
-        for _ in range(repeats):
+        for rep in range(repeats + warmup):
             table = BucketListHashTable(int(np.ceil(distinct / rho)), pool_slots,
                                         growth=GrowthPolicy(policy.initial_size, policy.factor),
                                         key_bits=spec.key_bits, group_width=group_width, workers=threads)
             secs, st = _timed(lambda: table.insert_device(dk, dv))
             _check_inserted(st, f"bucket-sweep {name}")
-            ins_secs += secs
+            ins_secs += secs if rep >= warmup else 0.0
             achieved = table.key_load_factor()
             secs, (off, flat) = _timed(lambda: table.retrieve_device(dq))
             offsets = off.cpu().numpy()
             _verify_multi(queries, offsets, _host_u64(flat), ref, f"bucket-sweep {name}")
             rbytes = _bucket_retrieve_bytes(np.diff(offsets))
-            ret_secs += secs
+            del off, flat
+            ret_secs += secs if rep >= warmup else 0.0
             del table
         for op, secs, b in (("insert", ins_secs, BUCKET_INSERT_BYTES * spec.n), ("retrieve", ret_secs, rbytes)):
             mean = secs / repeats
@@ -315,7 +320,7 @@ def run_bucket_sweep(policies: Sequence[str], spec: WorkloadSpec, *, group_width
 
 def run_distributed_sweep(shard_counts: Sequence[int], spec: WorkloadSpec, *, layout: str = "soa",
                           group_width: int = 32, threads: int = 1, repeats: int = 10,
-                          mode: ShardMode = ShardMode.DISTRIBUTED) -> list[BenchRecord]:
+                          mode: ShardMode = ShardMode.DISTRIBUTED, warmup: int = 1) -> list[BenchRecord]:
     """Multi-value shards (bench.py:305-359); shard s lives on GPU s mod (visible GPUs)."""
     keys = gen_multiplicity(spec)
     vals = np.arange(1, spec.n + 1, dtype=np.uint64)
@@ -331,19 +336,20 @@ def run_distributed_sweep(shard_counts: Sequence[int], spec: WorkloadSpec, *, la
         ins_secs = ret_secs = 0.0
         achieved = 0.0
         rbytes = 0.0
-        for _ in range(repeats):
+        for rep in range(repeats + warmup):
             with DistributedTable(shards, lambda s: MultiValueHashTable(
                     per_shard, layout=layout, key_bits=spec.key_bits, value_bits=vbits,
                     group_width=group_width, device=s % ngpu), mode=mode) as table:
                 secs, st = _timed(lambda: table.insert_device(dk, dv))
                 _check_inserted(st, f"distributed-sweep shards={shards}")
-                ins_secs += secs
+                ins_secs += secs if rep >= warmup else 0.0
                 achieved = sum(t.occupied for t in table.shards) / sum(t.capacity for t in table.shards)
                 secs, (off, flat) = _timed(lambda: table.retrieve_device(dq))
                 offsets = off.cpu().numpy()
                 _verify_multi(queries, offsets, _host_u64(flat), ref, f"distributed-sweep shards={shards}")
                 rbytes = _multi_retrieve_bytes(np.diff(offsets))
-                ret_secs += secs
+                del off, flat
+                ret_secs += secs if rep >= warmup else 0.0
         for op, secs, b in (("insert", ins_secs, INSERT_BYTES * spec.n), ("retrieve", ret_secs, rbytes)):
             mean = secs / repeats
             records.append(_record("distributed_multi", op, layout, group_width, spec.n, spec.r, rho, achieved,
@@ -380,6 +386,8 @@ def build_parser() -> argparse.ArgumentParser:
     common.add_argument("--key-bits", type=int, default=32, choices=(32, 64))
     common.add_argument("--seed", type=int, default=42)
     common.add_argument("--repeats", type=int, default=10, help="timed repetitions averaged per sweep point")
+    common.add_argument("--warmup", type=int, default=1,
+                        help="untimed repetitions first (allocator pools, module loading)")
     common.add_argument("--policies", default="default,optimal", help="comma list: default, optimal, or s0:growth")
     common.add_argument("--reference-columns", action="store_true",
                         help="write exactly the reference's CSV header (no GPU columns)")
@@ -401,16 +409,16 @@ def main(argv: Sequence[str] | None = None) -> int:
     try:
         if args.command == "single-sweep":
             records = run_single_sweep(args.densities, spec, layout=args.layout, group_width=args.group_width,
-                                       threads=args.threads, repeats=args.repeats)
+                                       threads=args.threads, repeats=args.repeats, warmup=args.warmup)
         elif args.command == "multi-sweep":
             records = run_multi_sweep(args.multiplicities, spec, layout=args.layout, group_width=args.group_width,
-                                      threads=args.threads, repeats=args.repeats)
+                                      threads=args.threads, repeats=args.repeats, warmup=args.warmup)
         elif args.command == "bucket-sweep":
             records = run_bucket_sweep([p for p in args.policies.split(",") if p], spec,
-                                       group_width=args.group_width, threads=args.threads, repeats=args.repeats)
+                                       group_width=args.group_width, threads=args.threads, repeats=args.repeats, warmup=args.warmup)
         else:
             records = run_distributed_sweep(args.shards, spec, layout=args.layout, group_width=args.group_width,
-                                            threads=args.threads, repeats=args.repeats)
+                                            threads=args.threads, repeats=args.repeats, warmup=args.warmup)
     except VerificationError as err:
         print(f"verification failed: {err}", file=sys.stderr)
         return 2

@@ -646,6 +646,37 @@ int ch_multi_retrieve(ch_table* t, const void* keys, uint64_t n, const uint64_t*
   return o.done(multi_scan(o.lc, t->T, t->ts, keys, n, nullptr, offsets, vals_out, 1, ll, lc2));
 }
 
+int ch_multi_retrieve_slots(ch_table* t, const void* keys, uint64_t n, const uint64_t* offsets, void* vals_out,
+                            int64_t* slots_out, void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  if (t->cfg.kind != CH_MULTI) return fail(CH_EINVAL, "ch_multi_retrieve_slots needs a multi-value table");
+  if (n && (!keys || !offsets || !vals_out || !slots_out)) return fail(CH_EINVAL, "null buffer");
+  Ordered o(t, stream);
+  t->host_ops += n;
+  Scratch sc(o.s);
+  uint32_t* ll = (uint32_t*)sc.get(n * 4 + 16);
+  unsigned long long* lc2 = (unsigned long long*)sc.get(16);
+  if (!ll || !lc2) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+  return o.done(multi_scan(o.lc, t->T, t->ts, keys, n, nullptr, offsets, vals_out, 1, ll, lc2, slots_out));
+}
+
+int ch_for_all(ch_table* t, void* keys_out, void* vals_out, int64_t* slots_out, uint64_t cap, uint64_t* d_count,
+               void* stream) {
+  if (!t) return fail(CH_EINVAL, "null table");
+  Ordered o(t, stream);
+  Scratch sc(o.s);
+  const size_t sb = for_all_scratch_bytes(t->T.c);
+  void* p = sc.get(sb);
+  if (!p) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+  return o.done(table_for_all(o.lc, t->T, t->ts, keys_out, vals_out, slots_out, cap, d_count, p, sb));
+}
+
+int ch_reduce_live(ch_table* t, uint64_t* d_out, void* stream) {
+  if (!t || !d_out) return fail(CH_EINVAL, "null argument");
+  Ordered o(t, stream);
+  return o.done(table_reduce(o.lc, t->T, t->ts, (unsigned long long*)d_out));
+}
+
 int ch_bucket_insert(ch_table* t, const void* keys, const void* vals, uint64_t n, uint8_t* status, void* stream) {
   if (!t) return fail(CH_EINVAL, "null table");
   if (t->cfg.kind != CH_BUCKET) return fail(CH_EINVAL, "ch_bucket_insert needs a bucket-list table");

@@ -157,7 +157,11 @@ int multi_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const v
                  uint64_t n, uint8_t* status);
 int multi_scan(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
                uint32_t* counts, const uint64_t* offsets, void* vals_out, int mode, uint32_t* long_list,
-               unsigned long long* counters);
+               unsigned long long* counters, int64_t* slot_out = nullptr);
+size_t for_all_scratch_bytes(uint64_t c);
+int table_for_all(const Launch& lc, const TableRef& T, const TypeSel& ts, void* keys_out, void* vals_out,
+                  int64_t* slots_out, uint64_t cap, uint64_t* d_count, void* scratch, size_t scratch_bytes);
+int table_reduce(const Launch& lc, const TableRef& T, const TypeSel& ts, unsigned long long* out);
 int exclusive_scan_u32(const Launch& lc, const uint32_t* counts, uint64_t n, uint64_t* out, void* scratch,
                        size_t scratch_bytes);
 size_t exclusive_scan_scratch_bytes(uint64_t n);

@@ -21,6 +21,7 @@
 #include <type_traits>
 
 #include "dispatch.cuh"
+#include "probe.cuh"
 
 namespace chb {
 
@@ -93,6 +94,7 @@ __device__ __forceinline__ void mg_store_value(const TableRef& T, uint64_t q, V 
 // Big groups first: their index list (m >= MG_BIG), so the longest walks start while the
 // table is emptiest and no hot key is left as the kernel's tail.
 constexpr uint32_t MG_BIG = 256;
+constexpr uint32_t MG_SMALL = 8;  // groups below this are placed a thread per group (k_mg_small)
 __global__ void k_mg_big(const uint32_t* __restrict__ gstart, const uint64_t* __restrict__ ngroups_p,
                          uint32_t* __restrict__ big, unsigned long long* __restrict__ nbig) {
   const uint64_t ng = *ngroups_p;
@@ -124,22 +126,13 @@ __global__ void __launch_bounds__(MG_THREADS) k_mg_place(TableRef T, const K* __
   const uint32_t ug = (uint32_t)g;
   const uint64_t ngroups = *ngroups_p, nbig = *nbig_p;
   long long ops = 0, att = 0, win = 0, occ = 0;
-  for (;;) {
-    unsigned long long gi = 0;
-    if (lane == 0) gi = atomicAdd(next, 1ull);
-    gi = __shfl_sync(0xffffffffu, gi, 0);
-    if (gi >= nbig + ngroups) break;
-    if (gi < nbig) {
-      gi = big[gi];
-    } else {
-      gi -= nbig;
-      if (gstart[gi + 1] - gstart[gi] >= MG_BIG) continue;  // done in the big-group phase
-    }
+  // one group: walk its key's sequence and claim m cells
+  auto place = [&](uint64_t gi) {
     const uint32_t base = gstart[gi], m = gstart[gi + 1] - base;
     const K k = sk[base];
     if (k == e || k == tomb) {  // INVALID_KEY, no accounting (multi_table.py:213-215)
       for (uint32_t x = lane; x < m; x += 32) status[pay_idx(sidx[base + x])] = ST_INVALID;
-      continue;
+      return;
     }
     const ProbeStart ps = probe_start(T, (uint64_t)k);
     uint64_t ws = ps.h;
@@ -220,6 +213,101 @@ __global__ void __launch_bounds__(MG_THREADS) k_mg_place(TableRef T, const K* __
       win += (long long)(lost * T.max_windows);
     }
     for (uint32_t x = placed + lane; x < m; x += 32) status[pay_idx(sidx[base + x])] = ST_TABLE_FULL;
+  };
+  // big groups first, one per grab (their walks are long: spread them over the warps)
+  for (;;) {
+    unsigned long long gi = 0;
+    if (lane == 0) gi = atomicAdd(next, 1ull);
+    gi = __shfl_sync(0xffffffffu, gi, 0);
+    if (gi >= nbig) break;
+    place(big[gi]);
+  }
+  // the rest in sorted order, 32 groups per grab: with few copies per key (r ~ 1) one
+  // grab per group made the shared counter the kernel's limit (16.7 M atomics on one word)
+  for (;;) {
+    unsigned long long g0 = 0;
+    if (lane == 0) g0 = atomicAdd(next + 2, 32ull);
+    g0 = __shfl_sync(0xffffffffu, g0, 0);
+    if (g0 >= ngroups) break;
+    const uint64_t g1 = g0 + 32 < ngroups ? g0 + 32 : ngroups;
+    for (uint64_t gi = g0; gi < g1; ++gi) {
+      const uint32_t m = gstart[gi + 1] - gstart[gi];
+      if (m < MG_BIG && m >= MG_SMALL) place(gi);  // big ones were placed above, small ones by k_mg_small
+    }
+  }
+  const long long v[4] = {ops, att, win, occ};
+  long long* const dst[4] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
+                             &T.ctr->occupied};
+  cta_add<4>(v, dst);
+}
+
+// Groups of fewer than MG_SMALL copies (all of them when keys are unique, r = 1): one
+// THREAD per group walks the sequence with 8-slot (64 B) spans and claims the group's cells
+// one after another -- a warp per group left 31 lanes idle per claimed cell and measured
+// 6.6 ms for 2^24 single-copy groups (latency-bound with ~9.5 K groups in flight).
+// A lost CAS re-reads the span from the lost cell (single_table.py:232-233 order).
+template <Layout LAY, typename K, typename V, typename P>
+__global__ void __launch_bounds__(MG_THREADS) k_mg_small(TableRef T, const K* __restrict__ sk,
+                                                         const P* __restrict__ sidx,
+                                                         const uint32_t* __restrict__ gstart,
+                                                         const uint64_t* __restrict__ ngroups_p,
+                                                         const V* __restrict__ vals, uint8_t* __restrict__ status,
+                                                         int g) {
+  using Pr = Probe<LAY, K, V, 8>;
+  using Ops = typename Pr::Ops;
+  const K e = (K)T.e, tomb = (K)T.t;
+  const uint32_t ug = (uint32_t)g;
+  const uint64_t ngroups = *ngroups_p;
+  long long ops = 0, att = 0, win = 0, occ = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t gi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; gi < ngroups; gi += stride) {
+    const uint32_t base = gstart[gi], m = gstart[gi + 1] - base;
+    if (m >= MG_SMALL) continue;
+    const K k = sk[base];
+    if (k == e || k == tomb) {
+      for (uint32_t x = 0; x < m; ++x) status[pay_idx(sidx[base + x])] = ST_INVALID;
+      continue;
+    }
+    const ProbeStart ps = probe_start(T, (uint64_t)k);
+    Cursor cur;
+    cur.init(ps.h);
+    uint32_t placed = 0;
+    bool exhausted = false;
+    while (placed < m) {
+      typename Pr::Step st;
+      Pr::load(T, cur, k, st);
+      uint32_t fm = st.em | st.tm;
+      bool lost = false;
+      while (fm && placed < m) {
+        const uint32_t u = lowest_bit(fm);
+        const P pv = sidx[base + placed];
+        const V val = sizeof(P) == 8 ? (V)(uint32_t)pv : vals[pay_idx(pv)];
+        bool won = false;
+        Ops::claim(T, st.base + u, ((st.em >> u) & 1u) ? e : tomb, k, val, true, &won);
+        if (!won) {  // another claimant took it: re-read from this cell
+          cur.o = Pr::offset_of(cur, st, u);
+          lost = true;
+          break;
+        }
+        att += (long long)(cur.attempts + chunk_end(Pr::offset_of(cur, st, u), ug));
+        win += (long long)cur.windows_seen;
+        ++placed;
+        fm &= fm - 1;
+      }
+      if (placed >= m) break;
+      if (!lost && !Pr::advance(T, cur, st, ps.step)) {
+        exhausted = true;
+        break;
+      }
+    }
+    ops += m;
+    occ += placed;
+    if (exhausted) {  // TABLE_FULL for the rest, whole budget walked (as k_mg_place)
+      const uint64_t left = m - placed;
+      att += (long long)(left * (uint64_t)T.max_windows * WINDOW);
+      win += (long long)(left * T.max_windows);
+      for (uint32_t x = placed; x < m; ++x) status[pay_idx(sidx[base + x])] = ST_TABLE_FULL;
+    }
   }
   const long long v[4] = {ops, att, win, occ};
   long long* const dst[4] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
@@ -274,13 +362,13 @@ static int mgroup_impl(const Launch& lc, const TableRef& T, int g, const K* keys
   void* scan = take(scan_b);
   uint32_t* gstart = (uint32_t*)take((n + 1) * 4);
   uint32_t* big = (uint32_t*)take((n + 1) * 4);
-  unsigned long long* next = (unsigned long long*)take(64);  // [0] work counter, [1] big groups
+  unsigned long long* next = (unsigned long long*)take(64);  // [0] big-group grab, [1] big groups, [2] grab
   if ((size_t)(q - static_cast<char*>(scratch)) > scratch_bytes) {
     set_error("grouped insert scratch too small");
     return -22;
   }
   int rc = cuda_check(cudaMemsetAsync(status, ST_INSERTED, n, lc.stream), "memset");
-  if (!rc) rc = cuda_check(cudaMemsetAsync(next, 0, 16, lc.stream), "memset");
+  if (!rc) rc = cuda_check(cudaMemsetAsync(next, 0, 24, lc.stream), "memset");  // big grab, nbig, small grab
   if (rc) return rc;
   const unsigned grid = (unsigned)(lc.sms * 8);
   k_mg_payload<P, V><<<grid, MG_THREADS, 0, lc.stream>>>(idx, vals, n);
@@ -303,6 +391,8 @@ static int mgroup_impl(const Launch& lc, const TableRef& T, int g, const K* keys
     cudaEventRecord(e0, lc.stream);
   k_mg_place<LAY, K, V, P><<<grid, MG_THREADS, 0, lc.stream>>>(T, sk, sidx, gstart, hoff + n, big, next + 1, next,
                                                                 vals, status, g, g_mw);
+  count_launch();
+  k_mg_small<LAY, K, V, P><<<grid, MG_THREADS, 0, lc.stream>>>(T, sk, sidx, gstart, hoff + n, vals, status, g);
   count_launch();
   if (e1) {
     cudaEventRecord(e1, lc.stream);

@@ -96,8 +96,8 @@ template <Layout LAY, typename K, typename V, int G, int MODE>
 __global__ void __launch_bounds__(256) k_multi_scan(TableRef T, const K* __restrict__ keys, uint64_t n,
                                                     uint32_t* __restrict__ counts,
                                                     const uint64_t* __restrict__ offsets,
-                                                    V* __restrict__ out, uint32_t budget,
-                                                    uint32_t* __restrict__ long_list,
+                                                    V* __restrict__ out, int64_t* __restrict__ slot_out,
+                                                    uint32_t budget, uint32_t* __restrict__ long_list,
                                                     unsigned long long* __restrict__ long_count) {
   using P = Probe<LAY, K, V, G>;
   using Ops = typename P::Ops;
@@ -153,7 +153,10 @@ __global__ void __launch_bounds__(256) k_multi_scan(TableRef T, const K* __restr
         uint64_t r = total;
         for (uint32_t m = km; m; m &= m - 1, ++r) {
           // a writer racing the counting pass: keep the segment length (:285-286)
-          if (r < want) out[base_off + r] = P::value(T, st, lowest_bit(m));
+          if (r < want) {
+            out[base_off + r] = P::value(T, st, lowest_bit(m));
+            if (slot_out) slot_out[base_off + r] = (int64_t)(st.base + lowest_bit(m));  // for_each (:299-328)
+          }
         }
       }
       total += (uint64_t)__popc(km);
@@ -215,6 +218,7 @@ template <Layout LAY, typename K, typename V, int MODE>
 __global__ void __launch_bounds__(256) k_multi_walk(TableRef T, const K* __restrict__ keys, uint64_t n,
                                                     uint32_t* __restrict__ counts,
                                                     const uint64_t* __restrict__ offsets, V* __restrict__ out,
+                                                    int64_t* __restrict__ slot_out,
                                                     unsigned long long* __restrict__ next, int g,
                                                     const uint32_t* __restrict__ list,
                                                     const unsigned long long* __restrict__ n_dev) {
@@ -280,7 +284,10 @@ __global__ void __launch_bounds__(256) k_multi_walk(TableRef T, const K* __restr
           const uint64_t r = total + __popc(km & below);
           uint64_t q = wsv[v] + lane;
           if (q >= T.c) q -= T.c;
-          if (r < want) out[base + r] = mw_value<LAY, K, V>(T, q, w[v]);  // racing writer: keep the length
+          if (r < want) {  // racing writer: keep the length
+            out[base + r] = mw_value<LAY, K, V>(T, q, w[v]);
+            if (slot_out) slot_out[base + r] = (int64_t)q;
+          }
         }
         total += __popc(km);
         if (em) {
@@ -322,29 +329,31 @@ struct MultiKernels {
   static constexpr uint32_t kBudget = 4;
   static int scan(const Launch& lc, const TableRef& T, const void* keys, uint64_t n, uint32_t* counts,
                   const uint64_t* offsets, void* out, int mode, uint32_t* long_list,
-                  unsigned long long* counters) {
+                  unsigned long long* counters, int64_t* slot_out) {
     if (n == 0) return 0;
     int rc = cuda_check(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), lc.stream), "memset");
     if (rc) return rc;
     if (mode == 0) {
       auto kern = k_multi_scan<LAY, K, V, G, 0>;
       rc = launch_chunked(lc, T, (const void*)kern, n, (chunk_for<K, V>()), [&](dim3 g, dim3 b) {
-        kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out, kBudget, long_list, counters);
+        kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out, slot_out, kBudget, long_list,
+                                     counters);
       });
     } else {
       auto kern = k_multi_scan<LAY, K, V, G, 1>;
       rc = launch_chunked(lc, T, (const void*)kern, n, (chunk_for<K, V>()), [&](dim3 g, dim3 b) {
-        kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out, kBudget, long_list, counters);
+        kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out, slot_out, kBudget, long_list,
+                                     counters);
       });
     }
     if (rc) return rc;
     const unsigned grid = (unsigned)(lc.sms * 8);
     if (mode == 0)
       k_multi_walk<LAY, K, V, 0><<<grid, 256, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out,
-                                                             counters + 1, G, long_list, counters);
+                                                             slot_out, counters + 1, G, long_list, counters);
     else
       k_multi_walk<LAY, K, V, 1><<<grid, 256, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out,
-                                                             counters + 1, G, long_list, counters);
+                                                             slot_out, counters + 1, G, long_list, counters);
     count_launch();
     return cuda_check(cudaGetLastError(), "multi walk");
   }
@@ -357,9 +366,10 @@ int multi_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const v
 }
 int multi_scan(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
                uint32_t* counts, const uint64_t* offsets, void* vals_out, int mode, uint32_t* long_list,
-               unsigned long long* counters) {
+               unsigned long long* counters, int64_t* slot_out) {
   return dispatch_types<MultiKernels>(ts, [&](auto tag) {
-    return decltype(tag)::type::scan(lc, T, keys, n, counts, offsets, vals_out, mode, long_list, counters);
+    return decltype(tag)::type::scan(lc, T, keys, n, counts, offsets, vals_out, mode, long_list, counters,
+                                     slot_out);
   });
 }
 

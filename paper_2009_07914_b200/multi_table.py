@@ -134,31 +134,45 @@ class MultiValueHashTable(_TableBase):
         return offsets.cpu().numpy().tolist(), _io.from_device(vals, self.value_bits).tolist()
 
     # -- callbacks (multi_table.py:299-339) ------------------------------------------
+    def retrieve_slots_device(self, keys, stream=None):
+        """Two-pass retrieval that also returns each value's slot (ch_multi_retrieve_slots):
+        (offsets int64[n+1], values, slots int64) on the device, values in probe order."""
+        k = self._keys(keys)
+        n = k.numel()
+        _, offsets = self.count_device(k, stream)
+        total = int(offsets[n].item()) if n else 0
+        dev = f"cuda:{self.device}"
+        vals = torch.zeros(total, dtype=_io.torch_dtype(self.value_bits), device=dev)
+        slots = torch.full((total,), -1, dtype=torch.int64, device=dev)
+        if n and total:
+            _lib.check(_lib.lib().ch_multi_retrieve_slots(self._dt.handle, k.data_ptr(), n, offsets.data_ptr(),
+                                                          vals.data_ptr(), slots.data_ptr(), self._stream(stream)),
+                       "multi retrieve slots")
+        return offsets, vals, slots
+
+    def for_each_device(self, keys, fn: Callable | None = None, stream=None):
+        """Every match of the queries as CUDA tensors (keys, values, slots), query-major and in
+        probe order within a query; with ``fn``, fn(keys, values, slots) on the device."""
+        k = self._keys(keys)
+        offsets, vals, slots = self.retrieve_slots_device(k, stream)
+        reps = torch.repeat_interleave(k, (offsets[1:] - offsets[:-1]))
+        return fn(reps, vals, slots) if fn is not None else (reps, vals, slots)
+
     def for_each(self, keys: Iterable[int], callback: Callable[[int, int, int], None]) -> None:
+        """callback(key, value, slot) per match (multi_table.py:299-328); matches and their
+        slots come from the device walk (ch_multi_retrieve_slots)."""
         keys = [k for k in keys if not self._is_sentinel(k)]
         if not keys:
             return
-        offsets, flat = self.retrieve_bulk(keys)
-        # slot indices of the matches: re-walk on the host view of the device cells
-        from .probing import probe_order
-        skeys, _ = self.slots._host()
-        e = self.sentinels.empty_key
-        for i, k in enumerate(keys):
-            seg = flat[offsets[i]:offsets[i + 1]]
-            if not seg:
-                continue
-            slots = []
-            for idx in probe_order(k, self.config):
-                cell = int(skeys[idx])
-                if cell == k:
-                    slots.append(idx)
-                    if len(slots) == len(seg):
-                        break
-                elif cell == e:
-                    break
-            for v, s in zip(seg, slots):
-                callback(k, v, s)
+        ks, vals, slots = self.for_each_device(keys)
+        for k, v, s in zip(_io.from_device(ks, self.key_bits).tolist(), _io.from_device(vals, self.value_bits).tolist(),
+                           slots.cpu().tolist()):
+            callback(k, v, s)
 
     def for_all(self, callback: Callable[[int, int, int], None]) -> None:
-        for i, k, v in self.slots.iter_items():
+        """callback(key, value, slot) per stored pair in slot order (multi_table.py:330-339),
+        enumerated on the device (ch_for_all)."""
+        keys, vals, slots = self.for_all_device()
+        for k, v, i in zip(_io.from_device(keys, self.key_bits).tolist(),
+                           _io.from_device(vals, self.value_bits).tolist(), slots.cpu().tolist()):
             callback(k, v, i)

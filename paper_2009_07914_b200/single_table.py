@@ -119,6 +119,33 @@ class _TableBase:
         s = self._dt.stats()
         return ProbeCounters(ops=int(s.ops), attempts=int(s.attempts), windows_visited=int(s.windows))
 
+    # -- device functors (single_table.py:412-429) -------------
+    def _cell_value_dtype(self) -> torch.dtype:
+        bits = 64 if self._kind == _lib.CH_BUCKET else self.value_bits  # bucket cells hold handles
+        return _io.torch_dtype(bits)
+
+    def for_all_device(self, fn: Callable | None = None, stream=None):
+        """The live cells (neither empty nor tombstone) in slot order, compacted on the
+        device by ch_for_all: CUDA tensors (keys, values, slots).  With ``fn``, returns
+        fn(keys, values, slots) -- a functor applied on the device (tensor ops or another
+        kernel) instead of one host callback per slot."""
+        n = self.occupied
+        dev = f"cuda:{self.device}"
+        keys = torch.empty(n, dtype=_io.torch_dtype(self.key_bits), device=dev)
+        vals = torch.empty(n, dtype=self._cell_value_dtype(), device=dev)
+        slots = torch.empty(n, dtype=torch.int64, device=dev)
+        _lib.check(_lib.lib().ch_for_all(self._dt.handle, keys.data_ptr(), vals.data_ptr(), slots.data_ptr(), n,
+                                         None, self._stream(stream)), "for_all")
+        return fn(keys, vals, slots) if fn is not None else (keys, vals, slots)
+
+    def reduce_live(self, stream=None) -> dict:
+        """Built-in device functors folded over the live cells in one pass (ch_reduce_live)."""
+        out = torch.empty(5, dtype=torch.int64, device=f"cuda:{self.device}")
+        _lib.check(_lib.lib().ch_reduce_live(self._dt.handle, out.data_ptr(), self._stream(stream)), "reduce")
+        c, sm, kx, mn, mx = (int(x) & ((1 << 64) - 1) for x in out.cpu().tolist())
+        return {"count": c, "value_sum": sm, "key_xor": kx, "min_value": mn if c else None,
+                "max_value": mx if c else None}
+
     def deferred_count(self) -> int:
         """Keys the staged-region pass (csrc/staged.cu) handed to the COPS probe kernels
         since the last reset_probe_counters() (window 0 could not decide them)."""
@@ -342,6 +369,20 @@ class SingleValueHashTable(_TableBase):
             if slot >= 0:
                 callback(k, val, slot)
 
+    def for_each_device(self, keys, fn: Callable | None = None, stream=None):
+        """The present queries as CUDA tensors (keys, values, slots), in query order; with
+        ``fn``, fn(keys, values, slots) runs on them on the device."""
+        k = self._keys(keys)
+        slots, _, _, vals = self.find_device(k, with_values=True, stream=stream)
+        hit = slots >= 0
+        out = (k[hit], vals[hit], slots[hit])
+        return fn(*out) if fn is not None else out
+
     def for_all(self, callback: Callable[[int, int, int], None]) -> None:
-        for i, k, v in self.slots.iter_items():
+        """callback(key, value, slot) per live cell in slot order (single_table.py:425-429);
+        the cells are enumerated on the device (ch_for_all), only the live ones cross."""
+        keys, vals, slots = self.for_all_device()
+        kb, vb = self.key_bits, self.value_bits
+        for k, v, i in zip(_io.from_device(keys, kb).tolist(), _io.from_device(vals, vb).tolist(),
+                           slots.cpu().tolist()):
             callback(k, v, i)
