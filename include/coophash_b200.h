@@ -229,6 +229,17 @@ int ch_dist_insert(ch_dist* d, const void* const* d_keys, const void* const* d_v
 int ch_dist_retrieve(ch_dist* d, const void* const* d_keys, const uint64_t* n, void* const* d_vals_out,
                      uint8_t* const* d_found, void* const* streams);
 
+/* ---- k-mer sketching for the index demo (kmer.py:63-137) ----
+ * d_text: sequence bytes (ASCII); n_windows windows, window w = d_text[d_win_start[w] ..
+ * + d_win_len[w]) tagged d_win_tag[w] (NULL: the window number); total_len = sum of the
+ * lengths.  Per window: the canonical 2-bit k-mers (k <= 32; bases other than A/C/G/T in
+ * either case reset the roll) reduced to the `sketch` distinct ones with the smallest
+ * (mix64(kmer), kmer), ascending.  Output packed in window order: d_kmers_out / d_tags_out
+ * (capacity n_windows * sketch), *d_count (device u64) = pairs written. */
+int ch_kmer_sketch(const uint8_t* d_text, const uint64_t* d_win_start, const uint32_t* d_win_len,
+                   const uint32_t* d_win_tag, uint64_t n_windows, uint64_t total_len, int k, uint32_t sketch,
+                   uint64_t* d_kmers_out, uint32_t* d_tags_out, uint64_t* d_count, int device, void* stream);
+
 /* ---- u32-permutation variants (batches < 2^32): half the index traffic of the u64 forms ---- */
 int ch_multi_split32(const void* d_keys, int key_bytes, const void* d_vals, int val_bytes, uint64_t n,
                      uint32_t shards, uint32_t* d_perm, uint64_t* d_offsets, void* d_keys_out, void* d_vals_out,

@@ -92,6 +92,7 @@ _SIGS = {
                                  C.POINTER(_P)]),
     "ch_dist_retrieve": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_U64), C.POINTER(_P), C.POINTER(_P),
                                    C.POINTER(_P)]),
+    "ch_kmer_sketch": (C.c_int, [_P, _P, _P, _P, _U64, _U64, C.c_int, C.c_uint32, _P, _P, _P, C.c_int, _P]),
     "ch_multi_split32": (C.c_int, [_P, C.c_int, _P, C.c_int, _U64, C.c_uint32, _P, _P, _P, _P,
                                    C.c_int, _P]),
     "ch_scatter32": (C.c_int, [_P, C.c_int, _P, _U64, _P, C.c_int, _P]),

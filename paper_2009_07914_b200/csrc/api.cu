@@ -64,6 +64,10 @@ int multi_insert_grouped(const Launch& lc, const TableRef& T, const TypeSel& ts,
                          uint64_t n, uint8_t* status, void* scratch, size_t scratch_bytes);
 int bucket_walk(const Launch& lc, const BucketRef& B, int vbytes, const uint64_t* handles, uint64_t n,
                 const uint64_t* offsets, void* out);
+int kmer_sketch(const Launch& lc, const uint8_t* text, const uint64_t* win_start, const uint32_t* win_len,
+                const uint32_t* win_tag, uint64_t n_windows, int k, uint32_t sketch, uint64_t* km_out,
+                uint32_t* tag_out, uint64_t* d_count, void* scratch, size_t scratch_bytes, uint64_t total_len);
+size_t kmer_scratch_bytes(uint64_t n_windows, uint32_t sketch, uint64_t total_len);
 
 }  // namespace chb
 
@@ -920,6 +924,29 @@ int ch_gather(const void* src, int elem_bytes, const uint64_t* perm, uint64_t n,
   if (n && (!src || !perm || !dst)) return fail(CH_EINVAL, "null buffer");
   DeviceGuard dev(device);
   return permute(plain_launch(device, stream), src, elem_bytes, perm, n, dst, false);
+}
+
+int ch_kmer_sketch(const uint8_t* text, const uint64_t* win_start, const uint32_t* win_len, const uint32_t* win_tag,
+                   uint64_t n_windows, uint64_t total_len, int k, uint32_t sketch, uint64_t* kmers_out,
+                   uint32_t* tags_out, uint64_t* d_count, int device, void* stream) {
+  if (k < 1 || k > 32) return fail(CH_EINVAL, "k must lie in [1, 32] (2 bits per base)");
+  if (sketch < 1) return fail(CH_EINVAL, "sketch_size must be >= 1");
+  if (n_windows == 0) {
+    if (d_count) {
+      DeviceGuard dev(device);
+      return check(cudaMemsetAsync(d_count, 0, 8, (cudaStream_t)stream), "count");
+    }
+    return CH_OK;
+  }
+  if (!text || !win_start || !win_len || !kmers_out) return fail(CH_EINVAL, "null buffer");
+  DeviceGuard dev(device);
+  Launch lc = plain_launch(device, stream);
+  Scratch sc(lc.stream);
+  const size_t sb = kmer_scratch_bytes(n_windows, sketch, total_len);
+  void* p = sc.get(sb);
+  if (!p) return fail(CH_ENOMEM, "scratch allocation failed");
+  return kmer_sketch(lc, text, win_start, win_len, win_tag, n_windows, k, sketch, kmers_out, tags_out, d_count, p, sb,
+                     total_len);
 }
 
 int ch_segment_copy(const void* src, int elem_bytes, const uint64_t* src_off, const uint64_t* idx, uint64_t n,

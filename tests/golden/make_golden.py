@@ -284,7 +284,45 @@ def gen_workloads():
     dump("workloads.json", out)
 
 
+def gen_kmer():
+    """Canonical k-mers, window sketches and read classification of the reference's k-mer
+    demo (kmer.py:63-137) on seeded random sequences with non-ACGT gaps, lower case and
+    short tails."""
+    from coophash import kmer as km
+    rng = random.Random(63)
+    alphabet = "ACGTACGTACGTACGTacgtN"
+
+    def seq(n):
+        return "".join(rng.choice(alphabet) for _ in range(n))
+
+    seqs = [seq(n) for n in (5, 17, 40, 127, 128, 129, 300, 1000, 2500)] + ["ACGT" * 40, "N" * 50, "acgtnACGT" * 30]
+    out = {"seqs": seqs, "cases": []}
+    for k, window, sketch in [(16, 128, 16), (5, 20, 4), (31, 64, 8), (32, 100, 3), (1, 8, 2), (11, 11, 100)]:
+        p = km.KmerParams(k=k, window=window, sketch_size=sketch)
+        out["cases"].append({
+            "k": k, "window": window, "sketch": sketch,
+            "canonical": [[str(x) for x in km.canonical_kmers(s_, k)] for s_ in seqs[:6]],
+            "sketches": [[str(x) for x in km.sketch_sequence(s_, p)] for s_ in seqs],
+        })
+    # an index of 6 references, classification of 8 reads (multi-value backend, 64-bit keys)
+    refs = [km.ReferenceRecord(target_id=i, sequence=seq(3000 + 700 * i)) for i in range(6)]
+    reads = []
+    for j in range(8):
+        r = refs[j % 6].sequence
+        a = rng.randrange(0, len(r) - 400)
+        reads.append(r[a:a + 250 + 20 * j] + seq(30))
+    reads.append(seq(500))
+    p = km.KmerParams()
+    table = km.make_backend("oa", km.expected_sketch_volume(refs, p))
+    inserted = km.build_index(refs, p, table)
+    out["index"] = {"refs": [r.sequence for r in refs], "reads": reads, "inserted": inserted,
+                    "volume": km.expected_sketch_volume(refs, p),
+                    "classify": [[list(x) for x in km.classify(r, p, table)] for r in reads]}
+    dump("kmer.json", out)
+
+
 if __name__ == "__main__":
+    gen_kmer()
     gen_probing()
     gen_single()
     gen_multi()
