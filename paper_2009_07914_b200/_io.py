@@ -77,32 +77,62 @@ def split_pairs(pairs) -> tuple[list, list]:
     return [k for k, _ in pairs], [v for _, v in pairs]
 
 
-def pipelined(device: int, inputs: list, outputs: list, run, chunk: int) -> None:
+class Staging:
+    """Persistent device staging buffers of one table's host-buffer pipeline (three chunk
+    slots per input stream), with an event per slot marking when its last op consumed it.
+
+    Reusing them across calls removes the whole-stream wait a freshly allocated buffer
+    needs: the next call's H2D copies wait only for the slot they overwrite, so the
+    copies of a retrieve_host overlap the kernels still running for the insert_host
+    issued before it."""
+
+    NB = 3
+
+    def __init__(self):
+        self._sets = {}
+
+    def get(self, device: int, chunk: int, dtypes: tuple):
+        key = (device, chunk, dtypes)
+        st = self._sets.get(key)
+        if st is None:
+            dev = torch.device("cuda", device)
+            bufs = [[torch.empty(chunk, dtype=dt, device=dev) for dt in dtypes] for _ in range(self.NB)]
+            free = [None] * self.NB
+            s_in = torch.cuda.Stream(dev)
+            s_in.wait_stream(torch.cuda.current_stream(dev))  # fresh memory: after its previous users
+            st = self._sets[key] = (bufs, free, s_in, torch.cuda.Stream(dev))
+        return st
+
+
+def pipelined(device: int, inputs: list, outputs: list, run, chunk: int, staging: Staging | None = None) -> None:
     """Stream host inputs through a device op in chunks: H2D copies, kernels and D2H
     copies of consecutive chunks overlap on three CUDA streams.
 
     inputs / outputs: equal-length pinned host tensors (outputs are filled in place).
     run(list_of_device_input_slices, stream) -> list of device outputs, one per output.
-    The caller's current stream waits for the whole pipeline before returning.
+    The caller's current stream waits for the whole pipeline (the D2H copies included)
+    when this returns; the host does not (callers synchronise when they need the data).
     """
     n = inputs[0].numel()
     if n == 0:
         return
     dev = torch.device("cuda", device)
     compute = torch.cuda.current_stream(dev)
-    s_in = torch.cuda.Stream(dev)
-    s_out = torch.cuda.Stream(dev)
-    nb = 3
-    bufs = [[torch.empty(min(chunk, n), dtype=x.dtype, device=dev) for x in inputs] for _ in range(nb)]
-    free = [torch.cuda.Event() for _ in range(nb)]
-    s_in.wait_stream(compute)
+    if staging is not None:
+        bufs, free, s_in, s_out = staging.get(device, min(chunk, n), tuple(x.dtype for x in inputs))
+    else:
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        bufs = [[torch.empty(min(chunk, n), dtype=x.dtype, device=dev) for x in inputs] for _ in range(3)]
+        free = [None] * 3
+        s_in.wait_stream(compute)   # fresh buffers: order after whatever last used the memory
+    nb = len(bufs)
     for c, lo in enumerate(range(0, n, chunk)):
         hi = min(n, lo + chunk)
         m = hi - lo
         b = c % nb
         ev_in = torch.cuda.Event()
         with torch.cuda.stream(s_in):
-            if c >= nb:
+            if free[b] is not None:
                 s_in.wait_event(free[b])
             for d, x in zip(bufs[b], inputs):
                 d[:m].copy_(x[lo:hi], non_blocking=True)
@@ -111,13 +141,14 @@ def pipelined(device: int, inputs: list, outputs: list, run, chunk: int) -> None
         outs = run([d[:m] for d in bufs[b]], compute)
         ev_done = torch.cuda.Event()
         ev_done.record(compute)
-        free[b].record(compute)  # the inputs are consumed once the op has run: the next H2D
-        with torch.cuda.stream(s_out):  # into this buffer need not wait for the D2H below
+        free[b] = ev_done  # the inputs are consumed once the op has run: the next H2D into
+        with torch.cuda.stream(s_out):  # this buffer need not wait for the D2H below
             s_out.wait_event(ev_done)
             for o, y in zip(outs, outputs):
                 o.record_stream(s_out)
                 y[lo:hi].copy_(o, non_blocking=True)
     compute.wait_stream(s_out)
-    for bb in bufs:
-        for d in bb:
-            d.record_stream(s_in)
+    if staging is None:
+        for bb in bufs:
+            for d in bb:
+                d.record_stream(s_in)

@@ -272,21 +272,25 @@ class SingleValueHashTable(_TableBase):
 
     # -- host-buffer bulk API (pipelined H2D / kernels / D2H) ---------------------
     def insert_host(self, keys, values, chunk: int | None = None,
-                    status_out: torch.Tensor | None = None) -> torch.Tensor:
+                    status_out: torch.Tensor | None = None, sync: bool = True) -> torch.Tensor:
         """Bulk insert from (pinned) host tensors; returns pinned host status codes.
-        Copies and kernels of consecutive chunks overlap (_io.pipelined); returns
-        once the statuses are on the host."""
+        Copies and kernels of consecutive chunks overlap (_io.pipelined).  ``sync=False``
+        returns at once: the statuses are valid after the device's current stream
+        synchronises (e.g. at the end of a following retrieve_host), and that call's
+        copies overlap this one's remaining kernels."""
         keys = _host_tensor(keys, self.key_bits)
         values = _host_tensor(values, self.value_bits)
         status = status_out if status_out is not None else \
             torch.empty(keys.numel(), dtype=torch.uint8, pin_memory=True)
         _io.pipelined(self.device, [keys, values], [status],
-                      lambda d, s: [self.insert_device(d[0], d[1], stream=s)], chunk or self._host_chunk())
-        torch.cuda.current_stream(self.device).synchronize()
+                      lambda d, s: [self.insert_device(d[0], d[1], stream=s)], chunk or self._host_chunk(),
+                      self._staging())
+        if sync:
+            torch.cuda.current_stream(self.device).synchronize()
         return status
 
     def retrieve_host(self, keys, chunk: int | None = None, values_out: torch.Tensor | None = None,
-                      found_out: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+                      found_out: torch.Tensor | None = None, sync: bool = True) -> tuple[torch.Tensor, torch.Tensor]:
         """Bulk retrieve for (pinned) host keys; returns pinned host (values, found)."""
         keys = _host_tensor(keys, self.key_bits)
         n = keys.numel()
@@ -294,9 +298,17 @@ class SingleValueHashTable(_TableBase):
             torch.empty(n, dtype=_io.torch_dtype(self.value_bits), pin_memory=True)
         found = found_out if found_out is not None else torch.empty(n, dtype=torch.uint8, pin_memory=True)
         _io.pipelined(self.device, [keys], [vals, found],
-                      lambda d, s: list(self.retrieve_device(d[0], stream=s)), chunk or self._host_chunk())
-        torch.cuda.current_stream(self.device).synchronize()
+                      lambda d, s: list(self.retrieve_device(d[0], stream=s)), chunk or self._host_chunk(),
+                      self._staging())
+        if sync:
+            torch.cuda.current_stream(self.device).synchronize()
         return vals, found
+
+    def _staging(self) -> "_io.Staging":
+        st = getattr(self, "_stage", None)
+        if st is None:
+            st = self._stage = _io.Staging()
+        return st
 
     def _host_chunk(self) -> int:
         # c/24 keys per chunk: short pipeline fill / drain, and each chunk still covers the

@@ -489,6 +489,17 @@ def test_host_pipeline_matches_device_path():
     assert f[:n].all() and (v[:n] == vals.astype(np.uint32)).all()
     dv, df = t.retrieve_device(keys[:4096])
     assert (dv.cpu().numpy().view(np.uint32) == v[:4096]).all()
+    # async insert_host then retrieve_host, repeatedly through the same staging buffers
+    from paper_2009_07914_b200 import _lib
+    import torch
+    for rep in range(3):
+        _lib.check(_lib.lib().ch_clear(t._dt.handle, torch.cuda.current_stream().cuda_stream))
+        kk = keys[rep::3]
+        vv = (vals[rep::3] + rep) % (1 << 32)
+        st = t.insert_host(kk, vv, chunk=1 << 18, sync=False)
+        v, f = t.retrieve_host(kk, chunk=1 << 18)
+        assert (st.numpy() == 0).all() and f.numpy().all()
+        assert (v.numpy().view(np.uint32) == vv.astype(np.uint32)).all()
 
 
 @pytest.mark.parametrize("switches", [{"CH_STAGED_ROUND2": "1", "CH_STAGED_FB_CTAS": "1"},
@@ -593,3 +604,41 @@ def test_staged_overflowing_partition_areas(skew):
     got = dict(zip(keys[single].tolist(), vv[single].tolist()))
     want = dict(zip(keys[single].tolist(), vals[single].astype(np.uint32).tolist()))
     assert got == want
+
+
+@pytest.mark.parametrize("rho", [0.9, 0.97])
+def test_staged_misses_and_erase_vs_direct(rho):
+    """Misses (absent keys walk until an empty, mostly past window 0 at high load) through
+    the fingerprint kernels agree with the word-scanning direct kernels on the same table
+    -- values, found flags and probe counters -- before and after an erase."""
+    n = 1 << 20
+    rng = np.random.default_rng(int(rho * 1000))
+    pool = rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=3 * n, dtype=np.uint64)))
+    present, absent = pool[:n], pool[n:2 * n]
+    t = SingleValueHashTable(int(n / rho), layout="packed", key_bits=32, value_bits=32, group_width=8)
+    t.set_locality("staged")
+    t.insert_device(present, present ^ np.uint64(7))
+    q = np.concatenate([absent, present[::3]])
+
+    def both(keys):
+        out = []
+        for mode in ("staged", "off"):
+            t.set_locality(mode)
+            t.reset_probe_counters()
+            v, f = t.retrieve_device(keys)
+            c = t.probe_counters()
+            out.append((v.cpu().numpy(), f.cpu().numpy(), (c.ops, c.attempts, c.windows_visited)))
+        return out
+
+    a, b = both(q)
+    for x, y in zip(a, b):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+    assert not a[1][:n].any() and a[1][n:].all()
+    er = t.erase_device(present[::5]).cpu().numpy()
+    assert er.all() and t.tombstones == er.size
+    a, b = both(np.concatenate([present, absent[:1000]]))
+    for x, y in zip(a, b):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+    gone = np.zeros(n, dtype=bool)
+    gone[::5] = True
+    assert (a[1][:n].astype(bool) == ~gone).all()
