@@ -38,8 +38,8 @@ int segment_copy(const Launch& lc, const void* src, int elem_bytes, const uint64
                  uint64_t n, const uint64_t* dst_off, void* dst);
 
 int bucket_insert(const Launch& lc, const BucketRef& B, const TypeSel& ts, const void* keys, const void* vals,
-                  uint64_t n, uint8_t* status, int64_t* slots, uint32_t* rank, uint64_t* need, uint64_t* alloc_off,
-                  void* scan_scratch, size_t scan_bytes);
+                  uint64_t n, uint8_t* status, void* scratch, size_t scratch_bytes);
+size_t bucket_insert_scratch_bytes(uint64_t n, uint64_t c);
 int bucket_counts(const Launch& lc, const uint64_t* handles, uint64_t n, uint32_t* counts);
 struct LocPlan {
   int shift;
@@ -688,17 +688,12 @@ int ch_bucket_insert(ch_table* t, const void* keys, const void* vals, uint64_t n
   if (n == 0) return CH_OK;
   Ordered o(t, stream);
   Scratch sc(o.s);
-  const uint64_t c = t->T.c;
-  const size_t sb = exclusive_scan_scratch_bytes(c + 1);
-  int64_t* slots = (int64_t*)sc.get(n * 8);
-  uint32_t* rank = (uint32_t*)sc.get(n * 4);
-  uint64_t* need = (uint64_t*)sc.get(c * 8);
-  uint64_t* alloc_off = (uint64_t*)sc.get((c + 1) * 8);
-  void* scan = sc.get(sb);
-  if (!slots || !rank || !need || !alloc_off || !scan) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+  const size_t sb = bucket_insert_scratch_bytes(n, t->T.c);  // O(min(batch, key store))
+  void* p = sc.get(sb);
+  if (!p) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
   TypeSel ts = t->ts;
   ts.vbytes = t->vbytes;  // arena value width for the write pass
-  return o.done(bucket_insert(o.lc, bucket_ref(t), ts, keys, vals, n, status, slots, rank, need, alloc_off, scan, sb));
+  return o.done(bucket_insert(o.lc, bucket_ref(t), ts, keys, vals, n, status, p, sb));
 }
 
 int ch_bucket_count(ch_table* t, const void* keys, uint64_t n, uint32_t* counts, uint64_t* offsets,

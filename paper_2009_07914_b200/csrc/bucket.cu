@@ -7,13 +7,18 @@
 // per batch with no contention:
 //   1. find_or_claim every key in the key store                (single.cu K1 MODE 1)
 //   2. rank[i] = atomicAdd(batch_count[slot])                  k_bucket_rank
-//   3. per key-store slot: how many values fit, how many arena
+//   3. the batch's distinct key-store slots (rank 0), compacted in batch order
+//      (flag + exclusive scan)                                 k_bucket_touch
+//   4. per touched slot: how many values fit, how many arena
 //      cells the new buckets need                              k_bucket_need
-//   4. exclusive scan of the needs -> contention-free bump offsets (prims.cu)
-//   5. per slot: carve its buckets, link the headers, publish the
+//   5. exclusive scan of the needs -> contention-free bump offsets (prims.cu)
+//   6. per touched slot: carve its buckets, link the headers, publish the
 //      new handle (READY, or FULL once the pool/count limit hits) k_bucket_alloc
 //      (pool exhaustion falls back to the reference's bucket-by-bucket order in
 //      k_bucket_alloc_seq, so OUT_OF_MEMORY stays per key and sticky)
+// Every pass is O(batch): steps 3-6 run over the touched-slot list, never over the
+// key store's capacity (an element insert into a 2^23-key store is a handful of tiny
+// launches, not three sweeps of the store).
 //   6. every pair writes its value at the arena cell its index maps to    k_bucket_write
 // The chain geometry is a pure function of the growth policy (:11-15), so the
 // arena cell of value index v is computed, never searched.
@@ -38,12 +43,32 @@ __global__ void k_bucket_rank(const int64_t* __restrict__ slots, uint64_t n, uin
   }
 }
 
-template <typename K>
-__global__ void k_bucket_need(BucketRef B, Layout lay, uint64_t* __restrict__ need_out) {
+// touched[pos[i]] = slots[i] for the first element of every slot (rank 0), batch order
+__global__ void k_bucket_flag(const int64_t* __restrict__ slots, const uint32_t* __restrict__ rank, uint64_t n,
+                              uint32_t* __restrict__ flag) {
   const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
-  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < B.T.c; s += stride) {
-    const uint32_t m = B.bcnt[s];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    flag[i] = (slots[i] >= 0 && rank[i] == 0) ? 1u : 0u;
+}
+__global__ void k_bucket_touch(const int64_t* __restrict__ slots, const uint32_t* __restrict__ flag,
+                               const uint64_t* __restrict__ pos, uint64_t n, uint64_t* __restrict__ touched) {
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    if (flag[i]) touched[pos[i]] = (uint64_t)slots[i];
+}
+
+// need_out[i] for entry i: touched-list entry i < d (*d_touched), 0 up to n (the scan runs
+// over n); without a list (touched == nullptr, batches larger than the key store) entry i
+// is key-store slot i, i < n = capacity, untouched slots need 0
+template <typename K>
+__global__ void k_bucket_need(BucketRef B, Layout lay, const uint64_t* __restrict__ touched,
+                              const uint64_t* __restrict__ d_touched, uint64_t n, uint64_t* __restrict__ need_out) {
+  const uint64_t d = touched ? *d_touched : n;
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     uint64_t need = 0;
+    const uint64_t s = touched ? (i < d ? touched[i] : 0) : i;
+    const uint32_t m = i < d ? B.bcnt[s] : 0u;
     if (m) {
       const uint64_t h = *handle_ptr<K>(B.T, lay, s);
       const uint64_t state = h >> (COUNT_BITS + TAIL_BITS), count = (h >> TAIL_BITS) & COUNT_MAX,
@@ -75,7 +100,7 @@ __global__ void k_bucket_need(BucketRef B, Layout lay, uint64_t* __restrict__ ne
       in.need = need;
       B.info[s] = in;
     }
-    need_out[s] = need;
+    need_out[i] = need;
   }
 }
 
@@ -96,12 +121,16 @@ __device__ __forceinline__ uint64_t link_buckets(const BucketRef& B, uint64_t re
 }
 
 template <typename K>
-__global__ void k_bucket_alloc(BucketRef B, Layout lay, const uint64_t* __restrict__ alloc_off, int vbytes) {
+__global__ void k_bucket_alloc(BucketRef B, Layout lay, const uint64_t* __restrict__ touched,
+                               const uint64_t* __restrict__ d_touched, const uint64_t* __restrict__ alloc_off,
+                               int vbytes) {
+  const uint64_t d = touched ? *d_touched : B.T.c;
   const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
   const unsigned long long bump0 = *B.bump;
   long long values = 0;
-  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < B.T.c; s += stride) {
-    if (!B.bcnt[s]) continue;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < d; i += stride) {
+    const uint64_t s = touched ? touched[i] : i;
+    if (!touched && !B.bcnt[s]) continue;
     BucketInfo in = B.info[s];
     uint64_t* hp = handle_ptr<K>(B.T, lay, s);
     const uint64_t h = *hp;
@@ -111,10 +140,10 @@ __global__ void k_bucket_alloc(BucketRef B, Layout lay, const uint64_t* __restri
     }
     uint64_t tail = in.tail_old;
     if (in.need) {
-      const uint64_t off = bump0 + alloc_off[s];
+      const uint64_t off = bump0 + alloc_off[i];
       if (off + in.need > B.pool_cap) {  // pool exhausted from here on: sequential fallback
         B.info[s].fit = FIT_DEFERRED;
-        atomicMin(B.first_fail, (unsigned long long)s);
+        atomicMin(B.first_fail, (unsigned long long)i);
         continue;
       }
       const uint64_t b0 = B.gr.buckets_for(in.c0);
@@ -133,22 +162,27 @@ __global__ void k_bucket_alloc(BucketRef B, Layout lay, const uint64_t* __restri
   cta_add<1>(v, dst);
 }
 
-// Pool exhausted: from the first failing slot on, allocate bucket by bucket in
-// slot order exactly like the reference's sequential appends (:252-255, :283-287).
+// Pool exhausted: from the first failing touched slot on (batch order of the keys' first
+// values), allocate bucket by bucket exactly like the reference's sequential appends
+// (:252-255, :283-287).
 template <typename K>
-__global__ void k_bucket_alloc_seq(BucketRef B, Layout lay, const uint64_t* __restrict__ alloc_off, int vbytes) {
+__global__ void k_bucket_alloc_seq(BucketRef B, Layout lay, const uint64_t* __restrict__ touched,
+                                   const uint64_t* __restrict__ d_touched, uint64_t n,
+                                   const uint64_t* __restrict__ alloc_off, int vbytes) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const unsigned long long ff = *B.first_fail;
   const unsigned long long bump0 = *B.bump;
+  const uint64_t d = touched ? *d_touched : B.T.c;
   if (ff == ~0ull) {  // everything fit: advance the bump by the total
-    *B.bump = bump0 + alloc_off[B.T.c];
-    B.T.ctr->pool_used += alloc_off[B.T.c];
+    *B.bump = bump0 + alloc_off[n];
+    B.T.ctr->pool_used += alloc_off[n];
     return;
   }
   uint64_t cursor = bump0 + alloc_off[ff];
   long long values = 0;
-  for (uint64_t s = ff; s < B.T.c; ++s) {
-    if (!B.bcnt[s] || B.info[s].fit != FIT_DEFERRED) continue;
+  for (uint64_t i = ff; i < d; ++i) {
+    const uint64_t s = touched ? touched[i] : i;
+    if ((!touched && !B.bcnt[s]) || B.info[s].fit != FIT_DEFERRED) continue;
     BucketInfo in = B.info[s];
     uint64_t* hp = handle_ptr<K>(B.T, lay, s);
     const uint64_t b0 = B.gr.buckets_for(in.c0);
@@ -279,9 +313,38 @@ __global__ void k_bucket_walk(BucketRef B, const uint64_t* __restrict__ handles,
 }
 
 // ------------------------------------------------------------ host side
+size_t bucket_insert_scratch_bytes(uint64_t n, uint64_t c) {
+  auto a = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const uint64_t m = n < c ? n : c;
+  return a(n * 8) + a(n * 4) + a(n * 4) + a((n + 1) * 8) + a(n * 8) + a(m * 8) + a((m + 1) * 8) +
+         a(exclusive_scan_scratch_bytes((n > m ? n : m) + 1)) + 256;
+}
+
 int bucket_insert(const Launch& lc, const BucketRef& B, const TypeSel& ts, const void* keys, const void* vals,
-                  uint64_t n, uint8_t* status, int64_t* slots, uint32_t* rank, uint64_t* need, uint64_t* alloc_off,
-                  void* scan_scratch, size_t scan_bytes) {
+                  uint64_t n, uint8_t* status, void* scratch, size_t scratch_bytes) {
+  char* q = static_cast<char*>(scratch);
+  auto take = [&](size_t b) {
+    char* r = q;
+    q += (b + 255) & ~(size_t)255;
+    return (void*)r;
+  };
+  // small batches work over the list of the slots they touch; batches of at least the
+  // key store's capacity sweep the slots instead (O(min(n, c)) either way)
+  const bool use_list = n < B.T.c;
+  const uint64_t m = use_list ? n : B.T.c;  // entries of the need / scan / alloc passes
+  int64_t* slots = (int64_t*)take(n * 8);
+  uint32_t* rank = (uint32_t*)take(n * 4);
+  uint32_t* flag = (uint32_t*)take(use_list ? n * 4 : 4);
+  uint64_t* pos = (uint64_t*)take(use_list ? (n + 1) * 8 : 8);  // pos[n] = touched slots
+  uint64_t* touched = (uint64_t*)take(use_list ? n * 8 : 8);
+  uint64_t* need = (uint64_t*)take(m * 8);
+  uint64_t* alloc_off = (uint64_t*)take((m + 1) * 8);
+  const size_t scan_bytes = exclusive_scan_scratch_bytes((n > m ? n : m) + 1);
+  void* scan_scratch = take(scan_bytes);
+  if ((size_t)(q - static_cast<char*>(scratch)) > scratch_bytes) {
+    set_error("bucket insert scratch too small");
+    return -22;
+  }
   const Layout lay = (Layout)ts.layout;
   TypeSel kts = ts;
   kts.vbytes = 8;  // key store values are 64-bit handles
@@ -290,26 +353,37 @@ int bucket_insert(const Launch& lc, const BucketRef& B, const TypeSel& ts, const
   rc = launch_persistent(lc, (const void*)k_bucket_rank, n, 1, [&](dim3 g, dim3 b) {
     k_bucket_rank<<<g, b, 0, lc.stream>>>(slots, n, B.bcnt, rank);
   });
+  if (use_list) {
+    if (!rc) rc = launch_persistent(lc, (const void*)k_bucket_flag, n, 1, [&](dim3 g, dim3 b) {
+      k_bucket_flag<<<g, b, 0, lc.stream>>>(slots, rank, n, flag);
+    });
+    if (!rc) rc = exclusive_scan_u32(lc, flag, n, pos, scan_scratch, scan_bytes);
+    if (!rc) rc = launch_persistent(lc, (const void*)k_bucket_touch, n, 1, [&](dim3 g, dim3 b) {
+      k_bucket_touch<<<g, b, 0, lc.stream>>>(slots, flag, pos, n, touched);
+    });
+  }
   if (rc) return rc;
+  const uint64_t* d_touched = use_list ? pos + n : nullptr;
+  if (!use_list) touched = nullptr;
   const bool k4 = ts.kbytes == 4;
   auto need_k = k4 ? (const void*)k_bucket_need<uint32_t> : (const void*)k_bucket_need<uint64_t>;
-  rc = launch_persistent(lc, need_k, B.T.c, 1, [&](dim3 g, dim3 b) {
-    if (k4) k_bucket_need<uint32_t><<<g, b, 0, lc.stream>>>(B, lay, need);
-    else k_bucket_need<uint64_t><<<g, b, 0, lc.stream>>>(B, lay, need);
+  rc = launch_persistent(lc, need_k, m, 1, [&](dim3 g, dim3 b) {
+    if (k4) k_bucket_need<uint32_t><<<g, b, 0, lc.stream>>>(B, lay, touched, d_touched, m, need);
+    else k_bucket_need<uint64_t><<<g, b, 0, lc.stream>>>(B, lay, touched, d_touched, m, need);
   });
   if (rc) return rc;
-  rc = exclusive_scan_u64(lc, need, B.T.c, alloc_off, scan_scratch, scan_bytes);
+  rc = exclusive_scan_u64(lc, need, m, alloc_off, scan_scratch, scan_bytes);
   if (rc) return rc;
   rc = cuda_check(cudaMemsetAsync(B.first_fail, 0xff, sizeof(unsigned long long), lc.stream), "memset");
   if (rc) return rc;
   auto alloc_k = k4 ? (const void*)k_bucket_alloc<uint32_t> : (const void*)k_bucket_alloc<uint64_t>;
-  rc = launch_persistent(lc, alloc_k, B.T.c, 1, [&](dim3 g, dim3 b) {
-    if (k4) k_bucket_alloc<uint32_t><<<g, b, 0, lc.stream>>>(B, lay, alloc_off, ts.vbytes);
-    else k_bucket_alloc<uint64_t><<<g, b, 0, lc.stream>>>(B, lay, alloc_off, ts.vbytes);
+  rc = launch_persistent(lc, alloc_k, m, 1, [&](dim3 g, dim3 b) {
+    if (k4) k_bucket_alloc<uint32_t><<<g, b, 0, lc.stream>>>(B, lay, touched, d_touched, alloc_off, ts.vbytes);
+    else k_bucket_alloc<uint64_t><<<g, b, 0, lc.stream>>>(B, lay, touched, d_touched, alloc_off, ts.vbytes);
   });
   if (rc) return rc;
-  if (k4) k_bucket_alloc_seq<uint32_t><<<1, 32, 0, lc.stream>>>(B, lay, alloc_off, ts.vbytes);
-  else k_bucket_alloc_seq<uint64_t><<<1, 32, 0, lc.stream>>>(B, lay, alloc_off, ts.vbytes);
+  if (k4) k_bucket_alloc_seq<uint32_t><<<1, 32, 0, lc.stream>>>(B, lay, touched, d_touched, m, alloc_off, ts.vbytes);
+  else k_bucket_alloc_seq<uint64_t><<<1, 32, 0, lc.stream>>>(B, lay, touched, d_touched, m, alloc_off, ts.vbytes);
   count_launch();
   rc = cuda_check(cudaGetLastError(), "bucket alloc seq");
   if (rc) return rc;
