@@ -244,6 +244,12 @@ int ch_kmer_sketch(const uint8_t* d_text, const uint64_t* d_win_start, const uin
 int ch_multi_split32(const void* d_keys, int key_bytes, const void* d_vals, int val_bytes, uint64_t n,
                      uint32_t shards, uint32_t* d_perm, uint64_t* d_offsets, void* d_keys_out, void* d_vals_out,
                      int device, void* stream);
+/* route + stable split returning the INVERSE map: d_pos[i] = split position of source
+ * element i (written in source order, coalesced), so results come back with a coalesced
+ * ch_gather32(results, d_pos) instead of a scatter's partial-line writes */
+int ch_route_split32(const void* d_keys, int key_bytes, const void* d_vals, int val_bytes, uint64_t n,
+                     uint32_t shards, uint32_t* d_pos, uint64_t* d_offsets, void* d_keys_out, void* d_vals_out,
+                     int device, void* stream);
 int ch_scatter32(const void* d_src, int elem_bytes, const uint32_t* d_perm, uint64_t n, void* d_dst, int device,
                  void* stream);
 int ch_gather32(const void* d_src, int elem_bytes, const uint32_t* d_perm, uint64_t n, void* d_dst, int device,

@@ -893,6 +893,21 @@ int ch_multi_split32(const void* keys, int key_bytes, const void* vals, int val_
                      vals_out, p, sb);
 }
 
+int ch_route_split32(const void* keys, int key_bytes, const void* vals, int val_bytes, uint64_t n, uint32_t shards,
+                     uint32_t* pos, uint64_t* offsets, void* keys_out, void* vals_out, int device, void* stream) {
+  if (!offsets || (n && (!keys || !pos))) return fail(CH_EINVAL, "null buffer");
+  if (key_bytes != 4 && key_bytes != 8) return fail(CH_EINVAL, "key_bytes must be 4 or 8");
+  if (vals && val_bytes != 4 && val_bytes != 8) return fail(CH_EINVAL, "val_bytes must be 4 or 8");
+  DeviceGuard dev(device);
+  Launch lc = plain_launch(device, stream);
+  Scratch sc(lc.stream);
+  const size_t sb = split_scratch_bytes(n, shards);
+  void* p = sc.get(sb);
+  if (!p) return fail(CH_ENOMEM, "scratch allocation failed");
+  return multi_split(lc, keys, key_bytes, vals, vals ? val_bytes : 4, n, shards, pos, -4, offsets, keys_out,
+                     vals_out, p, sb);
+}
+
 int ch_scatter32(const void* src, int elem_bytes, const uint32_t* perm, uint64_t n, void* dst, int device,
                  void* stream) {
   if (n && (!src || !perm || !dst)) return fail(CH_EINVAL, "null buffer");

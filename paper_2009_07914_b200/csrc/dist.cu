@@ -6,7 +6,7 @@
 // takes one batch per source device and runs, per source and per shard:
 //
 //   split      route + stable multi-split on the source device (K10, prims.cu):
-//              keys / values grouped by destination, u32 source index per position
+//              keys / values grouped by destination, u32 split position per source element
 //   counts     segment sizes to the host (the only host synchronisation of a call)
 //   exchange   every (source, shard) segment to its shard: NCCL grouped
 //              ncclSend / ncclRecv over NVLink (one group for keys + values), or
@@ -15,7 +15,7 @@
 //   local      ch_insert / ch_retrieve on each shard's own stream (staged regions
 //              when the received batch covers the shard)
 //   back       statuses / (value, found) back to the sources, same transport
-//   scatter    inverse permutation into the caller's order (K11)
+//   back-map   gather through the split's inverse map into the caller's order (K11)
 //
 // NCCL is dlopen'ed on first use ("libnccl.so.2": the copy torch already loaded,
 // else the system one), so single-GPU users of the library never need it.
@@ -252,7 +252,7 @@ int dist_op(ch_dist* D, bool insert, const void* const* keys, const void* const*
       return release(fail(CH_ENOMEM, "split scratch allocation failed"));
     DevGuard g(D->dev[s]);
     int rc = multi_split(launch_on(D->dev[s], ss[s]), keys[s], kb, insert ? vals[s] : nullptr, vb, n[s], S, perm[s],
-                         4, doff[s], kout[s], vout[s], scr, sb);
+                         -4, doff[s], kout[s], vout[s], scr, sb);  // perm[s][i] = split position of i
     if (!rc)
       rc = cuda_check(cudaMemcpyAsync(D->h_off + (size_t)s * (S + 1), doff[s], (S + 1) * 8, cudaMemcpyDeviceToHost,
                                       ss[s]),
@@ -329,11 +329,11 @@ int dist_op(ch_dist* D, bool insert, const void* const* keys, const void* const*
   for (int s = 0; s < S && !rc; ++s) {
     DevGuard g(D->dev[s]);
     const Launch lc = launch_on(D->dev[s], ss[s]);
-    if (insert) {
-      rc = permute32(lc, back_f[s], 1, perm[s], n[s], status[s], true);
+    if (insert) {  // gathers: coalesced writes in the source's order
+      rc = permute32(lc, back_f[s], 1, perm[s], n[s], status[s], false);
     } else {
-      rc = permute32(lc, back_v[s], vb, perm[s], n[s], vals_out[s], true);
-      if (!rc) rc = permute32(lc, back_f[s], 1, perm[s], n[s], found[s], true);
+      rc = permute32(lc, back_v[s], vb, perm[s], n[s], vals_out[s], false);
+      if (!rc) rc = permute32(lc, back_f[s], 1, perm[s], n[s], found[s], false);
     }
   }
   return release(rc);

@@ -176,16 +176,21 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const K* __restri
   for (uint32_t d = threadIdx.x; d < shards; d += SPLIT_THREADS) cnt[d] = 0;
   __syncthreads();
   const uint64_t base = blockIdx.x * SPLIT_TILE;
+  const unsigned lane = threadIdx.x & 31u;
   for (int r = 0; r < SPLIT_ROUNDS; ++r) {
     const uint64_t i = base + (uint64_t)r * SPLIT_THREADS + threadIdx.x;
-    if (i < n) atomicAdd(&cnt[route(keys[i], shards)], 1u);
+    const uint32_t d = i < n ? route(keys[i], shards) : shards;
+    // one shared atomic per destination present in the warp (few shards: 32 lanes on a
+    // handful of counters serialised the pass)
+    const unsigned m = __match_any_sync(0xffffffffu, d);
+    if (d < shards && lane == (unsigned)(__ffs(m) - 1)) atomicAdd(&cnt[d], (uint32_t)__popc(m));
   }
   __syncthreads();
   for (uint32_t d = threadIdx.x; d < shards; d += SPLIT_THREADS) hist[(uint64_t)d * gridDim.x + blockIdx.x] = cnt[d];
 }
 
 // stable scatter: rounds in input order, ranks within a round by warp then lane
-template <typename K, typename V, typename PI_T>
+template <typename K, typename V, typename PI_T, bool INV>
 __global__ void __launch_bounds__(SPLIT_THREADS) k_split_scatter(const K* __restrict__ keys,
                                                                 const V* __restrict__ vals, uint64_t n,
                                                                 uint32_t shards,
@@ -216,7 +221,8 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_scatter(const K* __rest
     if (valid) {
       uint64_t pos = run[d] + rank;
       for (int w = 0; w < warp; ++w) pos += wcnt[w][d];
-      perm[pos] = (PI_T)i;
+      if (INV) perm[i] = (PI_T)pos;  // source -> split position (coalesced)
+      else perm[pos] = (PI_T)i;
       if (keys_out) keys_out[pos] = key;
       if (vals_out) vals_out[pos] = vals[i];
     }
@@ -245,7 +251,7 @@ size_t split_scratch_bytes(uint64_t n, uint32_t shards) {
   return h * 4 + (h + 1) * 8 + scan_words_needed(h) * 8 + 256;
 }
 
-template <typename K, typename V, typename PI_T>
+template <typename K, typename V, typename PI_T, bool INV = false>
 static int split_impl(const Launch& lc, const K* keys, const V* vals, uint64_t n, uint32_t shards,
                       PI_T* perm, uint64_t* offsets, K* keys_out, V* vals_out, void* scratch,
                       size_t scratch_bytes) {
@@ -270,7 +276,7 @@ static int split_impl(const Launch& lc, const K* keys, const V* vals, uint64_t n
   if (rc) return rc;
   rc = exclusive_scan_u32(lc, hist, h, hist_off, scan_scratch, scratch_bytes - used);
   if (rc) return rc;
-  k_split_scatter<K, V, PI_T><<<(unsigned)tiles, SPLIT_THREADS, 0, lc.stream>>>(keys, vals, n, shards, hist_off, perm,
+  k_split_scatter<K, V, PI_T, INV><<<(unsigned)tiles, SPLIT_THREADS, 0, lc.stream>>>(keys, vals, n, shards, hist_off, perm,
                                                                          keys_out, vals_out);
   count_launch();
   rc = cuda_check(cudaGetLastError(), "split scatter");
@@ -283,11 +289,11 @@ static int split_impl(const Launch& lc, const K* keys, const V* vals, uint64_t n
 int multi_split(const Launch& lc, const void* keys, int kbytes, const void* vals, int vbytes, uint64_t n,
                 uint32_t shards, void* perm, int perm_bytes, uint64_t* offsets, void* keys_out, void* vals_out,
                 void* scratch, size_t scratch_bytes) {
-  if (perm_bytes != 4 && perm_bytes != 8) {
+  if (perm_bytes != 4 && perm_bytes != 8 && perm_bytes != -4) {  // -4: u32 inverse (source -> position)
     set_error("perm_bytes must be 4 or 8");
     return -22;
   }
-  if (perm_bytes == 4 && n > 0xFFFFFFFFull) {
+  if (perm_bytes != 8 && n > 0xFFFFFFFFull) {
     set_error("32-bit permutations need n < 2^32");
     return -22;
   }
@@ -297,7 +303,11 @@ int multi_split(const Launch& lc, const void* keys, int kbytes, const void* vals
   }
   if (!vals) vals_out = nullptr;
 #define CHB_SPLIT(K, V)                                                                                  \
-  return perm_bytes == 4                                                                                 \
+  return perm_bytes == -4                                                                                \
+             ? split_impl<K, V, uint32_t, true>(lc, (const K*)keys, (const V*)vals, n, shards,              \
+                                                (uint32_t*)perm, offsets, (K*)keys_out, (V*)vals_out,       \
+                                                scratch, scratch_bytes)                                     \
+         : perm_bytes == 4                                                                               \
              ? split_impl<K, V, uint32_t>(lc, (const K*)keys, (const V*)vals, n, shards, (uint32_t*)perm,   \
                                           offsets, (K*)keys_out, (V*)vals_out, scratch, scratch_bytes)     \
              : split_impl<K, V, uint64_t>(lc, (const K*)keys, (const V*)vals, n, shards, (uint64_t*)perm,   \

@@ -102,6 +102,31 @@ def split_device32(keys: torch.Tensor, num_shards: int, values: torch.Tensor | N
     return perm, offsets, kout, vout
 
 
+def route_split_device32(keys: torch.Tensor, num_shards: int, values: torch.Tensor | None = None, stream=None):
+    """Route + stable split returning the inverse map (ch_route_split32): pos[i] = split
+    position of element i.  Results come back with gather_device32(results, pos)."""
+    dev = keys.device.index
+    n = keys.numel()
+    pos = torch.empty(n, dtype=torch.int32, device=keys.device)
+    offsets = torch.empty(num_shards + 1, dtype=torch.int64, device=keys.device)
+    kout = torch.empty_like(keys)
+    vout = torch.empty_like(values) if values is not None else None
+    _lib.check(_lib.lib().ch_route_split32(
+        keys.data_ptr(), keys.element_size(), values.data_ptr() if values is not None else None,
+        values.element_size() if values is not None else 4, n, num_shards, pos.data_ptr(), offsets.data_ptr(),
+        kout.data_ptr(), vout.data_ptr() if vout is not None else None, dev,
+        _io.stream_of(dev, stream)), "route_split32")
+    return pos, offsets, kout, vout
+
+
+def gather_device32(src: torch.Tensor, pos: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """out[i] = src[pos[i]] (ch_gather32)."""
+    dev = src.device.index
+    _lib.check(_lib.lib().ch_gather32(src.data_ptr(), src.element_size(), pos.data_ptr(), out.numel(),
+                                      out.data_ptr(), dev, _io.stream_of(dev, stream)), "gather32")
+    return out
+
+
 def scatter_device32(src: torch.Tensor, perm: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
     """out[perm[i]] = src[i] with a u32 permutation (ch_scatter32)."""
     dev = src.device.index
@@ -530,12 +555,12 @@ class ShardedTable:
     insert_device / retrieve_device are collective: every rank calls them with its own
     batch (distributed.py:131-178, one process per GPU).  Pipeline per call:
 
-      split      route + stable split, u32 source index per position (K10, ch_multi_split32)
+      split      route + stable split, u32 split position per source element (K10, ch_route_split32)
       counts     one all_to_all of the S segment sizes (the only host synchronisation)
       exchange   keys (+ values) in ONE grouped send/recv (exchange_segments, NVLink)
       local      the shard's own insert / retrieve (staged regions for full-size batches)
       back       statuses / (values, found) in one grouped exchange
-      scatter    inverse u32 permutation into the caller's order (K11, ch_scatter32)
+      back-map   coalesced gather through that map into the caller's order (K11, ch_gather32)
     """
 
     def __init__(self, local_table, group=None):
@@ -564,17 +589,17 @@ class ShardedTable:
         v = self.table._vals(values)
         if k.numel() != v.numel():
             raise ValueError("keys and values differ in length")
-        perm, offsets, kout, vout = split_device32(k, self.world, v)
+        pos, offsets, kout, vout = route_split_device32(k, self.world, v)
         send, recv = self._counts(offsets)
         rk, rv = exchange_segments([kout, vout], send, recv, self.group)
         st = self.table.insert_device(rk, rv)
         (back,) = exchange_segments([st], recv, send, self.group)
         out = torch.empty(k.numel(), dtype=torch.uint8, device=k.device)
-        return scatter_device32(back, perm, out) if k.numel() else out
+        return gather_device32(back, pos, out) if k.numel() else out
 
     def retrieve_device(self, keys: torch.Tensor):
         k = self.table._keys(keys)
-        perm, offsets, kout, _ = split_device32(k, self.world)
+        pos, offsets, kout, _ = route_split_device32(k, self.world)
         send, recv = self._counts(offsets)
         (rk,) = exchange_segments([kout], send, recv, self.group)
         v, f = self.table.retrieve_device(rk)
@@ -583,6 +608,6 @@ class ShardedTable:
         vals = torch.empty(n, dtype=v.dtype, device=k.device)
         found = torch.empty(n, dtype=torch.uint8, device=k.device)
         if n:
-            scatter_device32(vb, perm, vals)
-            scatter_device32(fb, perm, found)
+            gather_device32(vb, pos, vals)
+            gather_device32(fb, pos, found)
         return vals, found

@@ -201,7 +201,8 @@ def test_sharded_table_world2_one_gpu():
 
 
 # ---------------------------------------------------------------- ch_dist_* (C ABI)
-from paper_2009_07914_b200.distributed import NativeDist, split_device32, scatter_device32  # noqa: E402
+from paper_2009_07914_b200.distributed import (NativeDist, gather_device32, route_split_device32,  # noqa: E402
+                                               scatter_device32, split_device32)
 
 
 @pytest.mark.parametrize("shards", [1, 2, 4, 8])
@@ -290,3 +291,22 @@ def test_split_of_empty_batch():
     assert offsets.cpu().tolist() == [0, 0, 0, 0, 0]
     perm, offsets, _, _ = split_device32(k.to(torch.int32), 3)
     assert offsets.cpu().tolist() == [0, 0, 0, 0]
+
+
+@pytest.mark.parametrize("shards", [1, 8, 37])
+def test_route_split32_inverse_and_gather(shards):
+    n = (1 << 20) + 33
+    rng = np.random.default_rng(90 + shards)
+    keys = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+    vals = rng.integers(0, 1 << 31, size=n, dtype=np.uint64).astype(np.uint32)
+    k = torch.from_numpy(keys.view(np.int32)).cuda()
+    v = torch.from_numpy(vals.view(np.int32)).cuda()
+    pos, offsets, kout, vout = route_split_device32(k, shards, v)
+    rperm, roff = orc.multi_split(keys.astype(np.uint64), shards)
+    inv = np.empty(n, dtype=np.int64)
+    inv[rperm] = np.arange(n)
+    assert (pos.cpu().numpy().view(np.uint32) == inv.astype(np.uint32)).all()
+    assert (offsets.cpu().numpy() == roff.astype(np.int64)).all()
+    assert (kout.cpu().numpy().view(np.uint32) == keys[rperm]).all()
+    back = gather_device32(vout, pos, torch.empty_like(v))
+    assert (back.cpu().numpy().view(np.uint32) == vals).all()
