@@ -934,6 +934,208 @@ __global__ void __launch_bounds__(RT, 2) k_st_probe(TableRef T, Part P,
   cta_add<6>(cv6, dst);
 }
 
+// Region pass for lookups, uniform rounds.  Every key of the region takes exactly one
+// 16-slot fingerprint step from window 0's start (thread i: the region's keys i, i + RT,
+// ...; coalesced key / lo loads one round ahead, coalesced result stores); a key the step
+// does not decide is pushed (warp-aggregated) to a shared queue with its offset, and the
+// queue is drained after the rounds with as many steps as each entry needs (a full window
+// ends at offset 32, so at most two more).  Same rule, results and counters as
+// k_st_probe<1, false>, without its per-step refill (ballot / shuffles / chunk cursors).
+//
+// Fingerprints here are 7 bits (fp7: 0..127) and an empty slot is 0x80, so one step flags
+// "the key's fingerprint or empty" with four integer ops per 4 slots (zero-byte test of
+// b ^ rep, OR the high bits of b), and the 16 per-slot flags are packed into one 16-bit
+// mask with two multiplies per 8 slots (flag_mask8), whose lowest set bit is the first
+// decisive slot.
+constexpr uint32_t LQ_CAP = 2048;  // queued keys per region (~8% of ~7.8 K at load 0.95)
+constexpr uint32_t FP_EMPTY = 0x80u;
+#ifndef CH_LQ_THREADS
+#define CH_LQ_THREADS 768
+#endif
+constexpr uint32_t LQT = CH_LQ_THREADS;  // lookup region CTA threads (2 CTAs per SM)
+
+__device__ __forceinline__ uint32_t fp7(uint32_t key) { return (key * 0x9E3779B1u) >> 25; }
+// bit 7 of each byte: the byte equals the key's fingerprint (rep = fp7 * 0x01010101) or is
+// empty; the lowest flag is exact (the zero-byte borrow only creates flags above a true one)
+__device__ __forceinline__ uint32_t fp_flags(uint32_t b, uint32_t rep) {
+  const uint32_t x = b ^ rep;
+  return ((x - 0x01010101u) & ~x & 0x80808080u) | (b & 0x80808080u);
+}
+// flags of slots 0..3 (f0) and 4..7 (f1) -> slot i at bit 24 + i.  Each product places
+// byte j's flag at 24 + j (f0 >> 4) or 28 + j (f1); every other partial-product bit lands
+// below bit 24 and no two partial products share a bit, so the sum carries nothing.
+__device__ __forceinline__ uint32_t flag_mask8(uint32_t f0, uint32_t f1) {
+  return (f0 >> 4) * 0x00204081u + f1 * 0x00204081u;
+}
+
+__global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, const uint32_t* __restrict__ keys,
+                                                       const uint16_t* __restrict__ los,
+                                                       uint32_t* __restrict__ res_val, uint8_t* __restrict__ res_flag,
+                                                       DeferOut DB, int g) {
+  constexpr uint32_t HALO = ST_HALO;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
+  uint32_t* fp32 = reinterpret_cast<uint32_t*>(tile + ST_R + HALO + TILE_PAD);
+  uint32_t* qk = fp32 + FP_BYTES / 4;  // queue: key, region index, lo | offset << 16
+  uint32_t* qi = qk + LQ_CAP;
+  uint32_t* qlo = qi + LQ_CAP;
+  __shared__ DeferBuf<false, DBUF_B> B;
+  __shared__ uint32_t s_qn;
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t f = blockIdx.x;
+  uint64_t k0;
+  uint32_t m;
+  if (P.foff) {
+    k0 = P.foff[f];
+    m = (uint32_t)(P.foff[f + 1] - k0);
+  } else {
+    k0 = (uint64_t)f * P.cr;
+    const uint32_t c2 = P.cur2[f], l2 = P.lim2[f];
+    m = c2 < l2 ? c2 : l2;
+  }
+  if (m == 0) return;
+  const uint64_t rbase = (uint64_t)f << ST_LOG_R;
+  const uint32_t len = (uint32_t)((T.c - rbase) < ST_R ? (T.c - rbase) : ST_R);
+  const uint64_t* slots = static_cast<const uint64_t*>(T.slots);
+  if (threadIdx.x == 0) {
+    B.n = 0;
+    s_qn = 0;
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, (len + HALO) * 8u);
+    bulk_load(tile, slots + rbase, len * 8u, &bar);
+    const uint64_t hb = rbase + len < T.c ? rbase + len : 0;
+    bulk_load(tile + len, slots + hb, HALO * 8u, &bar);
+  }
+  const uint32_t e = (uint32_t)T.e, t = (uint32_t)T.t;
+  const uint32_t gm = ~((uint32_t)g - 1u), ug = (uint32_t)g;
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t att = 0, ndef = 0, nsent = 0;
+  const uint32_t* const tw = reinterpret_cast<const uint32_t*>(tile);
+  const uint32_t* const kp = keys + k0;
+  const uint16_t* const lp = los + k0;
+  uint32_t* const rvp = res_val + k0;
+  uint8_t* const rfp = res_flag + k0;
+  const uint32_t k0u = (uint32_t)k0;
+  // first round's keys in flight while the tile lands
+  uint32_t nk = e, nl = 0;
+  if (threadIdx.x < m) {
+    nk = __ldcs(kp + threadIdx.x);
+    nl = __ldcs(lp + threadIdx.x);
+  }
+  __syncthreads();  // mbarrier initialised
+  mbar_wait(&bar, 0);
+  {
+    // 4 slots per thread from two 16-byte loads (consecutive threads, consecutive 32 B: no
+    // bank conflicts; a 4-byte key-word gather per slot was 8-way conflicted)
+    const uint32_t words = (len + HALO + TILE_PAD + 3) >> 2;
+    const uint4* t16 = reinterpret_cast<const uint4*>(tile);
+    for (uint32_t i = threadIdx.x; i < words; i += LQT) {
+      const uint4 a = t16[2 * i], b = t16[2 * i + 1];
+      const uint32_t w[4] = {a.x, a.z, b.x, b.z};
+      uint32_t fw = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) fw |= (w[u] == e ? FP_EMPTY : fp7(w[u])) << (8 * u);
+      fp32[i] = fw;
+    }
+    // past the staged slots: never decisive (a step only reads them beyond its window)
+    for (uint32_t i = words + threadIdx.x; i < FP_BYTES / 4; i += LQT) fp32[i] = 0x7F7F7F7Fu;
+  }
+  __syncthreads();
+
+  // one 16-slot step of key k (rep = fp7(k) * 0x01010101) at window offset o (updated);
+  // true while the key stays open
+  auto step = [&](uint32_t k, uint32_t rep, uint32_t lo, uint32_t i, uint32_t& o) -> bool {
+    const uint32_t x = lo + o, a = x >> 2, sh = (x & 3u) * 8u;
+    const uint32_t w0 = fp32[a], w1 = fp32[a + 1], w2 = fp32[a + 2], w3 = fp32[a + 3], w4 = fp32[a + 4];
+    const uint32_t f0 = fp_flags(__funnelshift_r(w0, w1, sh), rep);
+    const uint32_t f1 = fp_flags(__funnelshift_r(w1, w2, sh), rep);
+    const uint32_t f2 = fp_flags(__funnelshift_r(w2, w3, sh), rep);
+    const uint32_t f3 = fp_flags(__funnelshift_r(w3, w4, sh), rep);
+    const uint32_t mk = __byte_perm(flag_mask8(f0, f1), flag_mask8(f2, f3), 0x0073);  // slots 0..15 -> bits 0..15
+    const uint32_t u = (uint32_t)__ffs(mk) - 1u;  // first decisive slot (0xffffffff: none)
+    const uint32_t room = WINDOW - o;
+    if (u >= (room < 16u ? room : 16u)) {  // nothing decisive in this step's part of the window
+      o += 16u;
+      if (o < WINDOW) return true;
+      defer_push(B, DB, k, 0u, k0u + i, WINDOW);  // window 0 has neither the key nor an empty
+      ndef += 1;
+      return false;
+    }
+    o += u;
+    const uint32_t s2 = 2 * (lo + o);
+    const uint32_t c = tw[s2];
+    if (c != k && c != e) {  // fingerprint collision: scan on after it
+      o += 1;
+      if (o < WINDOW) return true;
+      defer_push(B, DB, k, 0u, k0u + i, WINDOW);
+      ndef += 1;
+      return false;
+    }
+    const bool hit = c == k;
+    rvp[i] = hit ? tw[s2 + 1] : 0u;
+    rfp[i] = (uint8_t)hit;
+    att += (o & gm) + ug;  // chunk_end(o, g)
+    return false;
+  };
+
+  for (uint32_t base = 0; base < m; base += LQT) {  // CTA-uniform rounds
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t k = nk, lo = nl;
+    if (i + LQT < m) {  // next round's keys
+      nk = __ldcs(kp + i + LQT);
+      nl = __ldcs(lp + i + LQT);
+    }
+    bool open = false;
+    uint32_t o = 0;
+    if (i < m) {
+      if (k == e || k == t) {  // sentinels are never stored (single_table.py:391-393)
+        rvp[i] = 0;
+        rfp[i] = 0;
+        nsent += 1;
+      } else {
+        open = step(k, fp7(k) * 0x01010101u, lo, i, o);
+      }
+    }
+    // warp-aggregated push of the open keys
+    const unsigned want = __ballot_sync(0xffffffffu, open);
+    if (want) {
+      const int leader = __ffs(want) - 1;
+      uint32_t qb = 0;
+      if ((int)lane == leader) qb = atomicAdd(&s_qn, (uint32_t)__popc(want));
+      qb = __shfl_sync(0xffffffffu, qb, leader);
+      if (open) {
+        const uint32_t s = qb + __popc(want & ((1u << lane) - 1u));
+        if (s < LQ_CAP) {
+          qk[s] = k;
+          qi[s] = i;
+          qlo[s] = lo | o << 16;
+        } else {  // queue full (skewed region): finish here
+          const uint32_t rep = fp7(k) * 0x01010101u;
+          while (step(k, rep, lo, i, o)) {
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t qn = s_qn < LQ_CAP ? s_qn : LQ_CAP;
+  for (uint32_t s = threadIdx.x; s < qn; s += LQT) {
+    const uint32_t k = qk[s], i = qi[s], w = qlo[s];
+    const uint32_t lo = w & 0xFFFFu, rep = fp7(k) * 0x01010101u;
+    uint32_t o = w >> 16;
+    while (step(k, rep, lo, i, o)) {
+    }
+  }
+  defer_flush(B, DB, true);  // syncs
+  // every key of the region is either resolved (one op, one window unless a sentinel) or deferred
+  const long long ops = (threadIdx.x == 0 ? (long long)m : 0ll) - (long long)ndef;
+  const long long cv6[6] = {ops, (long long)att, ops - (long long)nsent, 0ll, 0ll, (long long)ndef};
+  long long* const dst[6] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
+                             &T.ctr->occupied, nullptr, (long long*)&T.ctr->deferred};
+  cta_add<6>(cv6, dst);
+}
+constexpr size_t lookup_q_smem() { return (size_t)(ST_R + ST_HALO + TILE_PAD) * 8 + FP_BYTES + LQ_CAP * 12; }
+
 template <int MODE, bool R2>
 constexpr size_t probe_smem() {
   return (size_t)(ST_R + (MODE == 0 ? 0 : ST_HALO) + TILE_PAD) * 8 + (MODE == 0 ? 0 : FP_BYTES);
@@ -1092,6 +1294,12 @@ static int g_fb_blocks = [] {
   return v > 0 ? v : 0;
 }();
 
+// CH_PROBE_V1=1: the lane-refill region passes for every mode (A/B against the uniform rounds)
+static bool g_probe_v1 = [] {
+  const char* e = getenv("CH_PROBE_V1");
+  return e && e[0] == '1';
+}();
+
 size_t staged_scratch_bytes(const TableRef& T, uint64_t n, bool insert) {
   size_t total = 0;
   st_carve(st_plan(T, n), n, insert, g_round2, nullptr, &total);
@@ -1235,11 +1443,21 @@ template <int MODE, bool R2>
 static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const Round& r, const uint32_t* pos,
                     uint8_t* status, uint32_t* rv, uint8_t* rf, const DeferOut& DA, const DeferOut& DB, int g,
                     unsigned long long* exc = nullptr) {
+  cudaEvent_t e0;
+  if (MODE == 1 && !R2 && !g_probe_v1) {  // uniform rounds + queue (k_st_lookup_q)
+    const size_t sm = lookup_q_smem();
+    int rc = st_smem(k_st_lookup_q, sm);
+    if (rc) return rc;
+    st_timed(lc, &e0);
+    k_st_lookup_q<<<p.regions, LQT, sm, lc.stream>>>(T, r.part, r.k2, r.lo2, rv, rf, DB, g);
+    count_launch();
+    st_timed_end(lc, e0);
+    return cuda_check(cudaGetLastError(), "staged region lookup");
+  }
   const size_t sm = probe_smem<MODE, R2>();
   auto kern = k_st_probe<MODE, R2>;
   int rc = st_smem(kern, sm);
   if (rc) return rc;
-  cudaEvent_t e0;
   if (!R2) st_timed(lc, &e0);  // the dominant kernel of the staged schedule (bench.py roofline)
   kern<<<p.regions, RT, sm, lc.stream>>>(T, r.part, r.k2, MODE == 0 ? r.v2 : nullptr, pos, r.lo2, status, rv, rf,
                                          DA, DB, g, exc);
