@@ -1136,6 +1136,227 @@ __global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, cons
 }
 constexpr size_t lookup_q_smem() { return (size_t)(ST_R + ST_HALO + TILE_PAD) * 8 + FP_BYTES + LQ_CAP * 12; }
 
+// Region pass for inserts, uniform rounds (the insert counterpart of k_st_lookup_q).  The
+// fingerprint bytes are kept current while the region fills: a claim's winner turns its
+// slot's byte from empty (0x80) into the key's fp7 with one shared atomic XOR.  A byte can
+// lag its key word only between a CAS and that XOR, and a key that reads such a stale
+// "empty" loses the CAS exactly as if it had read the word -- a lost claim to another key
+// continues after the slot (single_table.py:232-233 re-reads, counted like it: + g
+// attempts), a lost claim to the same key is DUPLICATE_KEY (:224-231).  Tombstones are
+// 0x81 and decisive like an empty; a tombstone first defers the key to the COPS kernel
+// (the deferred-claim rule, :201-223), as in k_st_probe<0>.
+constexpr uint32_t IQ_CAP = 1536;  // queued keys per region
+constexpr uint32_t IQ_DBUF = 512;  // window-full deferrals buffered per region (~4.6% of ~7.8 K)
+constexpr uint32_t FP_TOMB = 0x81u;
+#ifndef CH_IQ_STEP
+#define CH_IQ_STEP 16
+#endif
+// slots per insert step.  32 (the whole window: a key claims as soon as it is examined)
+// measured 3.49 vs 3.00 ms; with 16 the queued keys (~20%) claim after the rest of the
+// region's keys, which leaves ~5-8% more keys past window 0 than the lane-refill pass did.
+constexpr uint32_t IQ_STEP = CH_IQ_STEP;
+
+__global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, const uint32_t* __restrict__ keys,
+                                                        const uint32_t* __restrict__ vals,
+                                                        const uint16_t* __restrict__ los,
+                                                        uint8_t* __restrict__ status, DeferOut DA, DeferOut DB, int g,
+                                                        unsigned long long* __restrict__ exc) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
+  uint32_t* fp32 = reinterpret_cast<uint32_t*>(tile + ST_R + TILE_PAD);
+  uint32_t* qk = fp32 + FP_BYTES / 4;  // queue: key, value, region index, lo | offset << 16
+  uint32_t* qv = qk + IQ_CAP;
+  uint32_t* qi = qv + IQ_CAP;
+  uint32_t* qlo = qi + IQ_CAP;
+  __shared__ DeferBuf<true, IQ_DBUF> B;  // -> DB (window full)
+  __shared__ DeferBuf<true, DBUF> BA;    // -> DA (tombstone first, window past the region)
+  __shared__ uint32_t s_qn;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int dirty;
+  const uint32_t f = blockIdx.x;
+  uint64_t k0;
+  uint32_t m;
+  if (P.foff) {
+    k0 = P.foff[f];
+    m = (uint32_t)(P.foff[f + 1] - k0);
+  } else {
+    k0 = (uint64_t)f * P.cr;
+    const uint32_t c2 = P.cur2[f], l2 = P.lim2[f];
+    m = c2 < l2 ? c2 : l2;
+  }
+  if (m == 0) return;
+  const uint64_t rbase = (uint64_t)f << ST_LOG_R;
+  const uint32_t len = (uint32_t)((T.c - rbase) < ST_R ? (T.c - rbase) : ST_R);
+  uint64_t* slots = static_cast<uint64_t*>(T.slots);
+  if (threadIdx.x == 0) {
+    B.n = 0;
+    BA.n = 0;
+    s_qn = 0;
+    dirty = 0;
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, len * 8u);
+    bulk_load(tile, slots + rbase, len * 8u, &bar);
+  }
+  const uint32_t e = (uint32_t)T.e, t = (uint32_t)T.t;
+  const uint32_t gm = ~((uint32_t)g - 1u), ug = (uint32_t)g;
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t att = 0, ndef = 0, nexc = 0, occ = 0, nsent = 0;
+  uint32_t* const tw = reinterpret_cast<uint32_t*>(tile);
+  const uint32_t* const kp = keys + k0;
+  const uint32_t* const vp = vals + k0;
+  const uint16_t* const lp = los + k0;
+  uint8_t* const stp = status + k0;
+  const uint32_t k0u = (uint32_t)k0;
+  uint32_t nk = e, nv = 0, nl = 0;
+  if (threadIdx.x < m) {
+    nk = __ldcs(kp + threadIdx.x);
+    nv = __ldcs(vp + threadIdx.x);
+    nl = __ldcs(lp + threadIdx.x);
+  }
+  __syncthreads();  // mbarrier initialised
+  mbar_wait(&bar, 0);
+  {
+    const uint32_t words = (len + TILE_PAD + 3) >> 2;
+    const uint4* t16 = reinterpret_cast<const uint4*>(tile);
+    for (uint32_t i = threadIdx.x; i < words; i += LQT) {
+      const uint4 a = t16[2 * i], b = t16[2 * i + 1];
+      const uint32_t w[4] = {a.x, a.z, b.x, b.z};
+      uint32_t fw = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) fw |= (w[u] == e ? FP_EMPTY : w[u] == t ? FP_TOMB : fp7(w[u])) << (8 * u);
+      fp32[i] = fw;
+    }
+    for (uint32_t i = words + threadIdx.x; i < FP_BYTES / 4; i += LQT) fp32[i] = 0x7F7F7F7Fu;
+  }
+  __syncthreads();
+
+  // one 16-slot step of key k at window offset o (updated); true while the key stays open
+  auto step = [&](uint32_t k, uint32_t v, uint32_t rep, uint32_t lo, uint32_t i, uint32_t& o) -> bool {
+    const uint32_t x = lo + o, a = x >> 2, sh = (x & 3u) * 8u;
+    uint32_t w[IQ_STEP / 4 + 1], fl[IQ_STEP / 4];
+#pragma unroll
+    for (int q = 0; q <= (int)IQ_STEP / 4; ++q) w[q] = lds32(fp32 + a + q);
+#pragma unroll
+    for (int q = 0; q < (int)IQ_STEP / 4; ++q) fl[q] = fp_flags(__funnelshift_r(w[q], w[q + 1], sh), rep);
+    uint32_t mk = __byte_perm(flag_mask8(fl[0], fl[1]), flag_mask8(fl[2], fl[3]), 0x0073);
+    if (IQ_STEP == 32)  // slots 16..31 -> bits 16..31
+      mk = (mk & 0xFFFFu) |
+           __byte_perm(flag_mask8(fl[4 % (IQ_STEP / 4)], fl[5 % (IQ_STEP / 4)]),
+                       flag_mask8(fl[6 % (IQ_STEP / 4)], fl[7 % (IQ_STEP / 4)]), 0x7300) & 0xFFFF0000u;
+    const uint32_t u = (uint32_t)__ffs(mk) - 1u;
+    const uint32_t room = WINDOW - o;
+    if (u >= (room < IQ_STEP ? room : IQ_STEP)) {
+      o += IQ_STEP;
+      if (o < WINDOW) return true;
+      defer_push(B, DB, k, v, k0u + i, WINDOW);  // neither the key nor a free cell in window 0
+      ndef += 1;
+      return false;
+    }
+    o += u;
+    const uint32_t s = lo + o;
+    const uint32_t c = lds32(tw + 2 * s);
+    if (c == t) {  // tombstone first: the deferred-claim rule, COPS kernel from window 0
+      defer_push(BA, DA, k, v, k0u + i, 0u);
+      ndef += 1;
+      return false;
+    }
+    if (c == e) {
+      const uint32_t old = atomicCAS(tw + 2 * s, e, k);
+      if (old == e) {
+        tw[2 * s + 1] = v;  // nothing in this pass reads values; the write-back follows a barrier
+        atomicXor(fp32 + (s >> 2), (FP_EMPTY ^ fp7(k)) << (8 * (s & 3u)));
+        occ += 1;
+        att += (o & gm) + ug;
+        return false;  // INSERTED is pre-set
+      }
+      if (old != k) {  // another key took the cell: on after it
+        att += ug;
+        o += 1;
+        if (o < WINDOW) return true;
+        defer_push(B, DB, k, v, k0u + i, WINDOW);
+        ndef += 1;
+        return false;
+      }
+    } else if (c != k) {  // fingerprint collision
+      o += 1;
+      if (o < WINDOW) return true;
+      defer_push(B, DB, k, v, k0u + i, WINDOW);
+      ndef += 1;
+      return false;
+    }
+    stp[i] = ST_DUPLICATE;  // present before the first free cell (single_table.py:198-200)
+    nexc += 1;
+    att += (o & gm) + ug;
+    return false;
+  };
+
+  for (uint32_t base = 0; base < m; base += LQT) {  // CTA-uniform rounds
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t k = nk, v = nv, lo = nl;
+    if (i + LQT < m) {
+      nk = __ldcs(kp + i + LQT);
+      nv = __ldcs(vp + i + LQT);
+      nl = __ldcs(lp + i + LQT);
+    }
+    bool open = false;
+    uint32_t o = 0;
+    if (i < m) {
+      if (k == e || k == t) {  // sentinels are never stored (single_table.py:369-370)
+        stp[i] = ST_INVALID;
+        nexc += 1;
+        nsent += 1;
+      } else if (lo + WINDOW > len) {  // the window leaves the staged region: COPS kernel
+        defer_push(BA, DA, k, v, k0u + i, 0u);
+        ndef += 1;
+      } else {
+        open = step(k, v, fp7(k) * 0x01010101u, lo, i, o);
+      }
+    }
+    const unsigned want = __ballot_sync(0xffffffffu, open);
+    if (want) {
+      const int leader = __ffs(want) - 1;
+      uint32_t qb = 0;
+      if ((int)lane == leader) qb = atomicAdd(&s_qn, (uint32_t)__popc(want));
+      qb = __shfl_sync(0xffffffffu, qb, leader);
+      if (open) {
+        const uint32_t q = qb + __popc(want & ((1u << lane) - 1u));
+        if (q < IQ_CAP) {
+          qk[q] = k;
+          qv[q] = v;
+          qi[q] = i;
+          qlo[q] = lo | o << 16;
+        } else {  // queue full: finish here
+          const uint32_t rep = fp7(k) * 0x01010101u;
+          while (step(k, v, rep, lo, i, o)) {
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t qn = s_qn < IQ_CAP ? s_qn : IQ_CAP;
+  for (uint32_t q = threadIdx.x; q < qn; q += LQT) {
+    const uint32_t k = qk[q], v = qv[q], i = qi[q], w = qlo[q];
+    const uint32_t lo = w & 0xFFFFu, rep = fp7(k) * 0x01010101u;
+    uint32_t o = w >> 16;
+    while (step(k, v, rep, lo, i, o)) {
+    }
+  }
+  defer_flush(B, DB, true);  // syncs
+  defer_flush(BA, DA, true);
+  if (occ) dirty = 1;
+  fence_smem_to_async();
+  __syncthreads();
+  if (threadIdx.x == 0 && dirty) bulk_store_wait(slots + rbase, tile, len * 8u);
+  // resolved keys: one op and one window each (sentinels: neither), deferred: counted by the COPS kernel
+  const long long ops = (threadIdx.x == 0 ? (long long)m : 0ll) - (long long)ndef - (long long)nsent;
+  const long long cv6[6] = {ops, (long long)att, ops, (long long)occ, (long long)nexc, (long long)ndef};
+  long long* const dst[6] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
+                             &T.ctr->occupied, (long long*)exc, (long long*)&T.ctr->deferred};
+  cta_add<6>(cv6, dst);
+}
+constexpr size_t insert_q_smem() { return (size_t)(ST_R + TILE_PAD) * 8 + FP_BYTES + IQ_CAP * 16; }
+
 template <int MODE, bool R2>
 constexpr size_t probe_smem() {
   return (size_t)(ST_R + (MODE == 0 ? 0 : ST_HALO) + TILE_PAD) * 8 + (MODE == 0 ? 0 : FP_BYTES);
@@ -1444,6 +1665,16 @@ static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const 
                     uint8_t* status, uint32_t* rv, uint8_t* rf, const DeferOut& DA, const DeferOut& DB, int g,
                     unsigned long long* exc = nullptr) {
   cudaEvent_t e0;
+  if (MODE == 0 && !R2 && !g_probe_v1) {  // uniform rounds + queue (k_st_insert_q)
+    const size_t sm = insert_q_smem();
+    int rc = st_smem(k_st_insert_q, sm);
+    if (rc) return rc;
+    st_timed(lc, &e0);
+    k_st_insert_q<<<p.regions, LQT, sm, lc.stream>>>(T, r.part, r.k2, r.v2, r.lo2, status, DA, DB, g, exc);
+    count_launch();
+    st_timed_end(lc, e0);
+    return cuda_check(cudaGetLastError(), "staged region insert");
+  }
   if (MODE == 1 && !R2 && !g_probe_v1) {  // uniform rounds + queue (k_st_lookup_q)
     const size_t sm = lookup_q_smem();
     int rc = st_smem(k_st_lookup_q, sm);
