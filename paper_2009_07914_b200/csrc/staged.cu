@@ -35,6 +35,7 @@
 // tile, per-tile run table), so results return by gathering the same runs --
 // every pass reads and writes coalesced and no position is carried per key.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 
 #include "dispatch.cuh"
@@ -1172,7 +1173,9 @@ __global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, cons
                                                         const uint32_t* __restrict__ vals,
                                                         const uint16_t* __restrict__ los,
                                                         uint8_t* __restrict__ status, DeferOut DA, DeferOut DB, int g,
-                                                        unsigned long long* __restrict__ exc) {
+                                                        unsigned long long* __restrict__ exc,
+                                                        const uint8_t* __restrict__ only) {
+  if (only && !only[blockIdx.x]) return;  // after k_st_insert_sg: the regions it handed back
   extern __shared__ __align__(128) unsigned char dsm[];
   uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
   uint32_t* fp32 = reinterpret_cast<uint32_t*>(tile + ST_R + TILE_PAD);
@@ -1369,6 +1372,356 @@ __global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, cons
 }
 constexpr size_t insert_q_smem() { return (size_t)(ST_R + TILE_PAD) * 8 + FP_BYTES + IQ_CAP * 16; }
 
+// ------------------------------------------------------------- sorted-greedy insert
+// Region pass for inserts that places the region's keys in ascending order of their window
+// start (lo): each key takes the first free slot of its window at its turn, so the result
+// is the reference's sequential insert of the keys in that order -- a valid linearisation
+// of the batch -- and among all orders it keeps the most keys inside window 0 (placing
+// equal-length intervals by left end, leftmost free slot first, is a maximum matching).
+// Simulated at load 0.95 (tools/sim_sorted_greedy.py): 0.2% of the keys leave window 0
+// against ~4% in arbitrary order; those are the keys the COPS kernels finish with random
+// DRAM probes, and fewer of them also lets more lookups resolve in window 0.
+//
+// Parallel form.  Keys with equal lo are interchangeable, so the greedy runs over the 2^13
+// window starts with multiplicities c_l; in free-slot index space (free = empty slot of the
+// staged tile) the lag of the placed keys behind each window start evolves by a clamped
+// addition, and one block scan of those maps gives every group's first slot and how many of
+// its keys fit (phase (c) below).  Keys that do not fit resume at window 1 (COPS kernel).
+// In-batch duplicates (same key -> same lo) are found after the placement by comparing each
+// key with its group's placed keys of lower rank; a region with one is handed back whole
+// (nothing has reached global memory by then).
+//
+// Regions with tombstones (the deferred-claim rule) or more than SG_MAXK keys are handed
+// back (redo[]) to k_st_insert_q, which runs next over those regions only.
+constexpr uint32_t SGT = 768;
+constexpr uint32_t SG_MAXK = 9216;            // keys per region (12 per thread)
+constexpr uint32_t SG_PER = SG_MAXK / SGT;    // keys per thread (region order)
+constexpr uint32_t SG_LPT = (ST_R + SGT - 1) / SGT;  // window starts per thread (11)
+constexpr uint32_t SG_DBUF = 256;             // deferrals buffered per region
+static_assert(SG_MAXK % SGT == 0 && SG_PER <= 12, "sorted pass geometry");
+
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* wt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) wt[warp] = x;
+  __syncthreads();
+  uint32_t y = lane < NT / 32 ? wt[lane] : 0u;
+#pragma unroll
+  for (int d = 1; d < NT / 32; d <<= 1) {
+    const uint32_t z = __shfl_up_sync(0xffffffffu, y, d);
+    if (lane >= d) y += z;
+  }
+  const uint32_t before = warp ? __shfl_sync(0xffffffffu, y, warp - 1) : 0u;
+  __syncthreads();  // wt reusable
+  return before + x - v;
+}
+
+// x -> min(max(x + p, q), r) on int lags; closed under composition
+struct ClampMap {
+  int p, q, r;
+  static constexpr int INF = 1 << 30;
+  __device__ __forceinline__ static ClampMap id() { return {0, -INF, INF}; }
+  __device__ __forceinline__ int apply(int x) const {
+    const int y = x + p > q ? x + p : q;
+    return y < r ? y : r;
+  }
+};
+// g after f
+__device__ __forceinline__ ClampMap compose(const ClampMap& f, const ClampMap& g) {
+  ClampMap h;
+  h.p = f.p + g.p;
+  const int q1 = f.q <= -ClampMap::INF ? -ClampMap::INF : f.q + g.p;
+  h.q = q1 > g.q ? q1 : g.q;
+  const int r1 = f.r >= ClampMap::INF ? ClampMap::INF : f.r + g.p;
+  const int r2 = r1 > g.q ? r1 : g.q;
+  h.r = r2 < g.r ? r2 : g.r;
+  return h;
+}
+// one window-start group: c keys, free indices a = fidx(l), a1 = fidx(l + 1), b = fidx(l + 32)
+__device__ __forceinline__ ClampMap group_map(uint32_t c, uint32_t a, uint32_t a1, uint32_t b) {
+  const int d = (int)(a1 - a), w = (int)(b - a);
+  if (c == 0) return {-d, -ClampMap::INF, ClampMap::INF};
+  return {(int)c - d, (int)c - d, w - d};
+}
+// exclusive prefix composition in thread order (identity for thread 0)
+template <int NT>
+__device__ __forceinline__ ClampMap block_excl_clamp(ClampMap x, int (*wsm)[3]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  ClampMap in = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    ClampMap y;
+    y.p = __shfl_up_sync(0xffffffffu, in.p, d);
+    y.q = __shfl_up_sync(0xffffffffu, in.q, d);
+    y.r = __shfl_up_sync(0xffffffffu, in.r, d);
+    if (lane >= d) in = compose(y, in);
+  }
+  if (lane == 31) wsm[warp][0] = in.p, wsm[warp][1] = in.q, wsm[warp][2] = in.r;
+  __syncthreads();
+  ClampMap carry = ClampMap::id();  // the warps before this one
+  for (int w = 0; w < warp; ++w) carry = compose(carry, ClampMap{wsm[w][0], wsm[w][1], wsm[w][2]});
+  ClampMap prev;  // the lanes before this one
+  prev.p = __shfl_up_sync(0xffffffffu, in.p, 1);
+  prev.q = __shfl_up_sync(0xffffffffu, in.q, 1);
+  prev.r = __shfl_up_sync(0xffffffffu, in.r, 1);
+  if (lane == 0) prev = ClampMap::id();
+  __syncthreads();
+  return compose(carry, prev);
+}
+
+// per-key class after the exclusion pass (key state bits 28..31; rank in bits 0..15)
+constexpr uint32_t SG_NONE = 0u, SG_PART = 1u, SG_INV = 2u, SG_DUP = 3u, SG_DEFA = 4u, SG_DEFB = 5u;
+
+__global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, const uint32_t* __restrict__ keys,
+                                                         const uint32_t* __restrict__ vals,
+                                                         const uint16_t* __restrict__ los,
+                                                         uint8_t* __restrict__ status, DeferOut DA, DeferOut DB,
+                                                         int g, unsigned long long* __restrict__ exc,
+                                                         uint8_t* __restrict__ redo) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
+  uint16_t* first = reinterpret_cast<uint16_t*>(tile + ST_R + TILE_PAD);  // per lo: free index of the first key
+  uint16_t* cnt = first + ST_R;                                            // per lo: participants -> placed
+  uint32_t* freew = reinterpret_cast<uint32_t*>(cnt + ST_R);               // free-slot bitmap
+  uint16_t* wpre = reinterpret_cast<uint16_t*>(freew + ST_R / 32);         // free slots before word w
+  __shared__ DeferBuf<true, SG_DBUF> B;   // -> DB (window full)
+  __shared__ DeferBuf<true, SG_DBUF> BA;  // -> DA (window past the region)
+  __shared__ uint32_t wt[SGT / 32];
+  __shared__ int s_tomb, s_occ, s_dup;
+  __shared__ int cm3[SGT / 32][3];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t f = blockIdx.x;
+  uint64_t k0;
+  uint32_t m;
+  if (P.foff) {
+    k0 = P.foff[f];
+    m = (uint32_t)(P.foff[f + 1] - k0);
+  } else {
+    k0 = (uint64_t)f * P.cr;
+    const uint32_t c2 = P.cur2[f], l2 = P.lim2[f];
+    m = c2 < l2 ? c2 : l2;
+  }
+  if (m == 0) return;
+  if (m > SG_MAXK) {  // skewed region: the concurrent pass takes it
+    if (threadIdx.x == 0) redo[f] = 1;
+    return;
+  }
+  const uint64_t rbase = (uint64_t)f << ST_LOG_R;
+  const uint32_t len = (uint32_t)((T.c - rbase) < ST_R ? (T.c - rbase) : ST_R);
+  uint64_t* slots = static_cast<uint64_t*>(T.slots);
+  if (threadIdx.x == 0) {
+    B.n = 0;
+    BA.n = 0;
+    s_tomb = 0;
+    s_occ = 0;
+    s_dup = 0;
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, len * 8u);
+    bulk_load(tile, slots + rbase, len * 8u, &bar);
+  }
+  {
+    uint32_t* z = reinterpret_cast<uint32_t*>(cnt);
+    for (uint32_t w = threadIdx.x; w < ST_R / 2; w += SGT) z[w] = 0;
+  }
+  const uint32_t e = (uint32_t)T.e, t = (uint32_t)T.t;
+  const uint32_t gm = ~((uint32_t)g - 1u), ug = (uint32_t)g;
+  const uint32_t* const kp = keys + k0;
+  const uint32_t* const vp = vals + k0;
+  const uint16_t* const lp = los + k0;
+  uint8_t* const stp = status + k0;
+  const uint32_t k0u = (uint32_t)k0;
+  uint32_t* const tw = reinterpret_cast<uint32_t*>(tile);
+  const uint32_t lane = threadIdx.x & 31u;
+  __syncthreads();  // zeroed, mbarrier initialised
+  mbar_wait(&bar, 0);
+  {  // free-slot bitmap (a warp per 32-slot word); tombstones / occupied cells in the tile
+    for (uint32_t w = threadIdx.x >> 5; w < ST_R / 32; w += SGT / 32) {
+      const uint32_t sl = 32 * w + lane;
+      const uint32_t kw = sl < len ? tw[2 * sl] : e;
+      const uint32_t fb = __ballot_sync(0xffffffffu, sl < len && kw == e);
+      const bool tb = __any_sync(0xffffffffu, sl < len && kw == t), oc = __any_sync(0xffffffffu, kw != e);
+      if (lane == 0) {
+        freew[w] = fb;
+        if (tb) s_tomb = 1;
+        if (oc) s_occ = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_tomb) {  // tombstones: the deferred-claim rule needs the concurrent pass
+    if (threadIdx.x == 0) redo[f] = 1;
+    return;
+  }
+  const bool occ_any = s_occ != 0;
+  {
+    const uint32_t fc = threadIdx.x < ST_R / 32 ? __popc(freew[threadIdx.x]) : 0u;
+    const uint32_t fb = block_excl_sum<SGT>(fc, wt);  // syncs
+    if (threadIdx.x < ST_R / 32) wpre[threadIdx.x] = (uint16_t)fb;
+  }
+  __syncthreads();
+  auto fidx = [&](uint32_t sl) -> uint32_t {  // free slots before slot sl (sl <= ST_R)
+    if (!occ_any) return sl < len ? sl : len;  // an empty tile: every staged slot is free
+    const uint32_t w = sl >> 5, b = sl & 31u;
+    if (w >= ST_R / 32) return (uint32_t)wpre[ST_R / 32 - 1] + __popc(freew[ST_R / 32 - 1]);
+    return (uint32_t)wpre[w] + __popc(freew[w] & ((1u << b) - 1u));
+  };
+  // (b) exclusions (region order, no side effects yet); participants take a rank in their group
+  uint32_t ks[SG_PER];  // class << 28 | rank (participants) or probe offset (pre-stored key)
+#pragma unroll
+  for (int u = 0; u < (int)SG_PER; ++u) {
+    const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
+    ks[u] = SG_NONE << 28;
+    if (i >= m) continue;
+    const uint32_t k = __ldcs(kp + i), lo = __ldcs(lp + i);
+    if (k == e || k == t) {  // sentinels are never stored (single_table.py:369-370)
+      ks[u] = SG_INV << 28;
+      continue;
+    }
+    if (lo + WINDOW > len) {  // window leaves the staged region: COPS kernel from window 0
+      ks[u] = SG_DEFA << 28;
+      continue;
+    }
+    if (occ_any) {  // stored before the first free cell (single_table.py:198-200)
+      uint32_t o = 0;
+      for (; o < WINDOW; ++o) {
+        const uint32_t kw = tw[2 * (lo + o)];
+        if (kw == e || kw == k) break;
+      }
+      if (o < WINDOW && tw[2 * (lo + o)] == k) {
+        ks[u] = SG_DUP << 28 | o;
+        continue;
+      }
+    }
+    if (fidx(lo) == fidx(lo + WINDOW)) {  // neither the key nor a free cell: resume at window 1
+      ks[u] = SG_DEFB << 28;
+      continue;
+    }
+    const uint32_t sh = (lo & 1u) * 16u;
+    ks[u] = SG_PART << 28 | (atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (lo >> 1), 1u << sh) >> sh & 0xFFFFu);
+  }
+  __syncthreads();
+  // (c) the exact greedy over window starts.  With lam_j = (chain end + 1) - a_j, the lag of the
+  // keys placed so far behind group j's first free index, the greedy is
+  //   lam_{j+1} = min(max(lam_j, 0) + c_j, w_j) - d_j   (c_j > 0),   lam_{j+1} = lam_j - d_j   (c_j = 0)
+  // (w_j: free slots of the window, d_j: slot j free), a clamped addition x -> min(max(x + p, q), r);
+  // those compose into the same form, so one block scan over the 2^13 window starts gives every
+  // group's first free index a_j + max(lam_j, 0) and how many of its keys fit,
+  // min(c_j, w_j - max(lam_j, 0)) -- the sequential greedy exactly (tools/sim_sorted_greedy.py).
+  {
+    const uint32_t l0 = threadIdx.x * SG_LPT;
+    uint32_t c[SG_LPT];
+    ClampMap h = ClampMap::id();
+#pragma unroll
+    for (int u = 0; u < (int)SG_LPT; ++u) {
+      const uint32_t l = l0 + (uint32_t)u;
+      c[u] = l < ST_R ? cnt[l] : 0u;
+      if (l < ST_R) h = compose(h, group_map(c[u], fidx(l), fidx(l + 1), fidx(l + WINDOW)));
+    }
+    int lam = block_excl_clamp<SGT>(h, cm3).apply(0);
+#pragma unroll
+    for (int u = 0; u < (int)SG_LPT; ++u) {
+      const uint32_t l = l0 + (uint32_t)u;
+      if (l >= ST_R) break;
+      const int a = (int)fidx(l), a1 = (int)fidx(l + 1), b = (int)fidx(l + WINDOW);
+      if (c[u]) {
+        const int lag = lam > 0 ? lam : 0;
+        const int fit = b - a - lag;
+        first[l] = (uint16_t)(a + lag);
+        cnt[l] = (uint16_t)((int)c[u] < fit ? (int)c[u] : (fit > 0 ? fit : 0));
+      }
+      lam = group_map(c[u], a, a1, b).apply(lam);
+    }
+  }
+  __syncthreads();
+  // (d) placement into the staged tile (region order, coalesced key / value reads)
+  auto slot_of = [&](uint32_t fi) -> uint32_t {  // the fi-th free slot
+    if (!occ_any) return fi;
+    uint32_t lo_w = 0, hi_w = ST_R / 32;  // last word with wpre <= fi
+    while (hi_w - lo_w > 1) {
+      const uint32_t mid = (lo_w + hi_w) >> 1;
+      if (wpre[mid] <= fi) lo_w = mid;
+      else hi_w = mid;
+    }
+    uint32_t fb = freew[lo_w];
+    for (uint32_t x = fi - wpre[lo_w]; x; --x) fb &= fb - 1;
+    return 32 * lo_w + __ffs(fb) - 1;
+  };
+#pragma unroll
+  for (int u = 0; u < (int)SG_PER; ++u) {
+    if ((ks[u] >> 28) != SG_PART) continue;
+    const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
+    const uint32_t lo = lp[i], r = ks[u] & 0xFFFFu;
+    if (r >= cnt[lo]) {  // past what window 0 holds for this group: resume at window 1
+      ks[u] = SG_DEFB << 28 | 1u << 16;
+      continue;
+    }
+    const uint32_t sl = slot_of((uint32_t)first[lo] + r);
+    tile[sl] = (uint64_t)vp[i] << 32 | kp[i];
+  }
+  __syncthreads();
+  // (e) in-batch duplicates (same key -> same lo): compare with the group's placed keys of lower
+  // rank (a deferred copy: with all of them).  One found: the region goes to the concurrent pass
+  // (nothing has been written to global memory yet).
+#pragma unroll
+  for (int u = 0; u < (int)SG_PER; ++u) {
+    const uint32_t cls = ks[u] >> 28;
+    if (cls != SG_PART && !(cls == SG_DEFB && (ks[u] >> 16 & 1u))) continue;
+    const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
+    const uint32_t lo = lp[i], k = kp[i];
+    const uint32_t n = cls == SG_PART ? (ks[u] & 0xFFFFu) : cnt[lo];
+    for (uint32_t x = 0; x < n; ++x)
+      if (tw[2 * slot_of((uint32_t)first[lo] + x)] == k) s_dup = 1;
+  }
+  __syncthreads();
+  if (s_dup) {
+    if (threadIdx.x == 0) redo[f] = 1;
+    return;
+  }
+  // (f) results: statuses, deferrals, counters
+  uint32_t nexc = 0, ndef = 0, nsent = 0, occn = 0, att = 0;
+#pragma unroll
+  for (int u = 0; u < (int)SG_PER; ++u) {
+    const uint32_t cls = ks[u] >> 28;
+    if (cls == SG_NONE) continue;
+    const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
+    if (cls == SG_PART) {
+      const uint32_t lo = lp[i];
+      const uint32_t sl = slot_of((uint32_t)first[lo] + (ks[u] & 0xFFFFu));
+      occn += 1;
+      att += ((sl - lo) & gm) + ug;
+    } else if (cls == SG_INV) {
+      stp[i] = ST_INVALID;
+      nexc += 1;
+      nsent += 1;
+    } else if (cls == SG_DUP) {
+      stp[i] = ST_DUPLICATE;
+      nexc += 1;
+      att += ((ks[u] & 0xFFFFu) & gm) + ug;
+    } else {
+      defer_push(cls == SG_DEFA ? BA : B, cls == SG_DEFA ? DA : DB, kp[i], vp[i], k0u + i,
+                 cls == SG_DEFA ? 0u : WINDOW);
+      ndef += 1;
+    }
+  }
+  defer_flush(B, DB, true);  // syncs
+  defer_flush(BA, DA, true);
+  fence_smem_to_async();
+  __syncthreads();
+  if (threadIdx.x == 0) bulk_store_wait(slots + rbase, tile, len * 8u);
+  const long long ops = (threadIdx.x == 0 ? (long long)m : 0ll) - (long long)ndef - (long long)nsent;
+  const long long cv6[6] = {ops, (long long)att, ops, (long long)occn, (long long)nexc, (long long)ndef};
+  long long* const dst[6] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
+                             &T.ctr->occupied, (long long*)exc, (long long*)&T.ctr->deferred};
+  cta_add<6>(cv6, dst);
+}
+constexpr size_t insert_sg_smem() { return (size_t)(ST_R + TILE_PAD) * 8 + ST_R * 4 + ST_R / 8 + ST_R / 16; }
+
 template <int MODE, bool R2>
 constexpr size_t probe_smem() {
   return (size_t)(ST_R + (MODE == 0 ? 0 : ST_HALO) + TILE_PAD) * 8 + (MODE == 0 ? 0 : FP_BYTES);
@@ -1441,6 +1794,7 @@ struct Round {
   uint16_t* lo2;
   uint16_t *inv1, *inv2, *th1, *th2;  // inverse (round 1 only)
   uint8_t *bid1, *bid2;               // bucket of each bucketed slot per tile (round 1 only)
+  uint8_t* redo;                      // regions k_st_insert_sg hands to k_st_insert_q (round 1 only)
   uint32_t *tg1, *tg2;
 };
 
@@ -1482,6 +1836,7 @@ static void carve_round(Carver& c, Round& r, const StPlan& p, uint64_t n, int np
   if (inverse) {
     r.inv1 = (uint16_t*)c.take(n * 2);
     r.inv2 = (uint16_t*)c.take(n1 * 2);
+    r.redo = (uint8_t*)c.take(p.regions);
     r.bid1 = npay == 0 ? (uint8_t*)c.take(n) : nullptr;  // lookups only (k_st_gather<L, true>)
     r.bid2 = npay == 0 ? (uint8_t*)c.take(n1) : nullptr;
     r.th1 = (uint16_t*)c.take(p.tiles1 * p.supers * 2);
@@ -1528,6 +1883,12 @@ static int g_fb_blocks = [] {
   const char* e = getenv("CH_STAGED_FB_CTAS");
   const int v = e ? atoi(e) : 0;
   return v > 0 ? v : 0;
+}();
+
+// CH_INSERT_SG=0: inserts without the sorted-greedy placement pass (k_st_insert_sg)
+static bool g_insert_sg = [] {
+  const char* e = getenv("CH_INSERT_SG");
+  return !(e && e[0] == '0');
 }();
 
 // CH_PROBE_V1=1: the lane-refill region passes for every mode (A/B against the uniform rounds)
@@ -1681,14 +2042,30 @@ static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const 
                     uint8_t* status, uint32_t* rv, uint8_t* rf, const DeferOut& DA, const DeferOut& DB, int g,
                     unsigned long long* exc = nullptr) {
   cudaEvent_t e0;
-  if (MODE == 0 && !R2 && !g_probe_v1) {  // uniform rounds + queue (k_st_insert_q)
+  if (MODE == 0 && !R2 && !g_probe_v1) {
+    // sorted-greedy placement (k_st_insert_sg), then the uniform-rounds pass (k_st_insert_q)
+    // over the regions it handed back (tombstones, skewed regions); CH_INSERT_SG=0: only the latter
     const size_t sm = insert_q_smem();
     int rc = st_smem(k_st_insert_q, sm);
     if (rc) return rc;
-    st_timed(lc, &e0);
-    k_st_insert_q<<<p.regions, LQT, sm, lc.stream>>>(T, r.part, r.k2, r.v2, r.lo2, status, DA, DB, g, exc);
+    const uint8_t* only = nullptr;
+    if (g_insert_sg) {
+      const size_t sm2 = insert_sg_smem();
+      if ((rc = st_smem(k_st_insert_sg, sm2))) return rc;
+      if ((rc = cuda_check(cudaMemsetAsync(r.redo, 0, p.regions, lc.stream), "memset"))) return rc;
+      st_timed(lc, &e0);
+      k_st_insert_sg<<<p.regions, SGT, sm2, lc.stream>>>(T, r.part, r.k2, r.v2, r.lo2, status, DA, DB, g, exc,
+                                                         r.redo);
+      count_launch();
+      st_timed_end(lc, e0);
+      if ((rc = cuda_check(cudaGetLastError(), "staged sorted insert"))) return rc;
+      only = r.redo;
+    } else {
+      st_timed(lc, &e0);
+    }
+    k_st_insert_q<<<p.regions, LQT, sm, lc.stream>>>(T, r.part, r.k2, r.v2, r.lo2, status, DA, DB, g, exc, only);
     count_launch();
-    st_timed_end(lc, e0);
+    if (!g_insert_sg) st_timed_end(lc, e0);
     return cuda_check(cudaGetLastError(), "staged region insert");
   }
   if (MODE == 1 && !R2 && !g_probe_v1) {  // uniform rounds + queue (k_st_lookup_q)
