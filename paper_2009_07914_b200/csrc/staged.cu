@@ -1538,6 +1538,14 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   const uint32_t k0u = (uint32_t)k0;
   uint32_t* const tw = reinterpret_cast<uint32_t*>(tile);
   const uint32_t lane = threadIdx.x & 31u;
+  // the region's keys and window starts (coalesced), in flight while the tile lands
+  uint32_t kk[SG_PER], ks0[SG_PER];
+#pragma unroll
+  for (int u = 0; u < (int)SG_PER; ++u) {
+    const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
+    kk[u] = i < m ? __ldcs(kp + i) : 0u;
+    ks0[u] = i < m ? (uint32_t)__ldcs(lp + i) : 0u;
+  }
   __syncthreads();  // zeroed, mbarrier initialised
   mbar_wait(&bar, 0);
   {  // free-slot bitmap (a warp per 32-slot word); tombstones / occupied cells in the tile
@@ -1571,14 +1579,15 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     if (w >= ST_R / 32) return (uint32_t)wpre[ST_R / 32 - 1] + __popc(freew[ST_R / 32 - 1]);
     return (uint32_t)wpre[w] + __popc(freew[w] & ((1u << b) - 1u));
   };
-  // (b) exclusions (region order, no side effects yet); participants take a rank in their group
-  uint32_t ks[SG_PER];  // class << 28 | rank (participants) or probe offset (pre-stored key)
+  // (b) exclusions (region order, no side effects yet); participants take a rank in their group.
+  // Key state ks: class << 28 | over-placed flag << 27 | lo << 14 | rank (or probe offset).
+  uint32_t ks[SG_PER];
 #pragma unroll
   for (int u = 0; u < (int)SG_PER; ++u) {
     const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
     ks[u] = SG_NONE << 28;
     if (i >= m) continue;
-    const uint32_t k = __ldcs(kp + i), lo = __ldcs(lp + i);
+    const uint32_t k = kk[u], lo = ks0[u];
     if (k == e || k == t) {  // sentinels are never stored (single_table.py:369-370)
       ks[u] = SG_INV << 28;
       continue;
@@ -1594,16 +1603,17 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
         if (kw == e || kw == k) break;
       }
       if (o < WINDOW && tw[2 * (lo + o)] == k) {
-        ks[u] = SG_DUP << 28 | o;
+        ks[u] = SG_DUP << 28 | lo << 14 | o;
         continue;
       }
     }
     if (fidx(lo) == fidx(lo + WINDOW)) {  // neither the key nor a free cell: resume at window 1
-      ks[u] = SG_DEFB << 28;
+      ks[u] = SG_DEFB << 28 | lo << 14;
       continue;
     }
     const uint32_t sh = (lo & 1u) * 16u;
-    ks[u] = SG_PART << 28 | (atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (lo >> 1), 1u << sh) >> sh & 0xFFFFu);
+    const uint32_t rk = atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (lo >> 1), 1u << sh) >> sh & 0xFFFFu;
+    ks[u] = SG_PART << 28 | lo << 14 | (rk < 0x3FFFu ? rk : 0x3FFFu);
   }
   __syncthreads();
   // (c) the exact greedy over window starts.  With lam_j = (chain end + 1) - a_j, the lag of the
@@ -1615,31 +1625,30 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   // min(c_j, w_j - max(lam_j, 0)) -- the sequential greedy exactly (tools/sim_sorted_greedy.py).
   {
     const uint32_t l0 = threadIdx.x * SG_LPT;
-    uint32_t c[SG_LPT];
     ClampMap h = ClampMap::id();
 #pragma unroll
     for (int u = 0; u < (int)SG_LPT; ++u) {
       const uint32_t l = l0 + (uint32_t)u;
-      c[u] = l < ST_R ? cnt[l] : 0u;
-      if (l < ST_R) h = compose(h, group_map(c[u], fidx(l), fidx(l + 1), fidx(l + WINDOW)));
+      if (l < ST_R) h = compose(h, group_map(cnt[l], fidx(l), fidx(l + 1), fidx(l + WINDOW)));
     }
     int lam = block_excl_clamp<SGT>(h, cm3).apply(0);
 #pragma unroll
     for (int u = 0; u < (int)SG_LPT; ++u) {
       const uint32_t l = l0 + (uint32_t)u;
       if (l >= ST_R) break;
+      const uint32_t c = cnt[l];
       const int a = (int)fidx(l), a1 = (int)fidx(l + 1), b = (int)fidx(l + WINDOW);
-      if (c[u]) {
+      if (c) {
         const int lag = lam > 0 ? lam : 0;
         const int fit = b - a - lag;
         first[l] = (uint16_t)(a + lag);
-        cnt[l] = (uint16_t)((int)c[u] < fit ? (int)c[u] : (fit > 0 ? fit : 0));
+        cnt[l] = (uint16_t)((int)c < fit ? (int)c : (fit > 0 ? fit : 0));
       }
-      lam = group_map(c[u], a, a1, b).apply(lam);
+      lam = group_map(c, a, a1, b).apply(lam);
     }
   }
   __syncthreads();
-  // (d) placement into the staged tile (region order, coalesced key / value reads)
+  // (d) placement into the staged tile; values load four keys at a time
   auto slot_of = [&](uint32_t fi) -> uint32_t {  // the fi-th free slot
     if (!occ_any) return fi;
     uint32_t lo_w = 0, hi_w = ST_R / 32;  // last word with wpre <= fi
@@ -1653,30 +1662,38 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     return 32 * lo_w + __ffs(fb) - 1;
   };
 #pragma unroll
-  for (int u = 0; u < (int)SG_PER; ++u) {
-    if ((ks[u] >> 28) != SG_PART) continue;
-    const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
-    const uint32_t lo = lp[i], r = ks[u] & 0xFFFFu;
-    if (r >= cnt[lo]) {  // past what window 0 holds for this group: resume at window 1
-      ks[u] = SG_DEFB << 28 | 1u << 16;
-      continue;
+  for (int g4 = 0; g4 < (int)SG_PER; g4 += 4) {
+    uint32_t vv[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int u = g4 + x;
+      vv[x] = (ks[u] >> 28) == SG_PART ? __ldcs(vp + threadIdx.x + (uint32_t)u * SGT) : 0u;
     }
-    const uint32_t sl = slot_of((uint32_t)first[lo] + r);
-    tile[sl] = (uint64_t)vp[i] << 32 | kp[i];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int u = g4 + x;
+      if ((ks[u] >> 28) != SG_PART) continue;
+      const uint32_t lo = (ks[u] >> 14) & 0x1FFFu, r = ks[u] & 0x3FFFu;
+      if (r >= cnt[lo]) {  // past what window 0 holds for this group: resume at window 1
+        ks[u] = SG_DEFB << 28 | 1u << 27 | lo << 14;
+        continue;
+      }
+      const uint32_t sl = slot_of((uint32_t)first[lo] + r);
+      tile[sl] = (uint64_t)vv[x] << 32 | kk[u];
+    }
   }
   __syncthreads();
   // (e) in-batch duplicates (same key -> same lo): compare with the group's placed keys of lower
-  // rank (a deferred copy: with all of them).  One found: the region goes to the concurrent pass
-  // (nothing has been written to global memory yet).
+  // rank (an over-placed copy: with all of them).  One found: the region goes to the concurrent
+  // pass (nothing has been written to global memory yet).
 #pragma unroll
   for (int u = 0; u < (int)SG_PER; ++u) {
     const uint32_t cls = ks[u] >> 28;
-    if (cls != SG_PART && !(cls == SG_DEFB && (ks[u] >> 16 & 1u))) continue;
-    const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
-    const uint32_t lo = lp[i], k = kp[i];
-    const uint32_t n = cls == SG_PART ? (ks[u] & 0xFFFFu) : cnt[lo];
+    if (cls != SG_PART && !(cls == SG_DEFB && (ks[u] >> 27 & 1u))) continue;
+    const uint32_t lo = (ks[u] >> 14) & 0x1FFFu;
+    const uint32_t n = cls == SG_PART ? (ks[u] & 0x3FFFu) : cnt[lo];
     for (uint32_t x = 0; x < n; ++x)
-      if (tw[2 * slot_of((uint32_t)first[lo] + x)] == k) s_dup = 1;
+      if (tw[2 * slot_of((uint32_t)first[lo] + x)] == kk[u]) s_dup = 1;
   }
   __syncthreads();
   if (s_dup) {
@@ -1690,9 +1707,9 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     const uint32_t cls = ks[u] >> 28;
     if (cls == SG_NONE) continue;
     const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
+    const uint32_t lo = (ks[u] >> 14) & 0x1FFFu;
     if (cls == SG_PART) {
-      const uint32_t lo = lp[i];
-      const uint32_t sl = slot_of((uint32_t)first[lo] + (ks[u] & 0xFFFFu));
+      const uint32_t sl = slot_of((uint32_t)first[lo] + (ks[u] & 0x3FFFu));
       occn += 1;
       att += ((sl - lo) & gm) + ug;
     } else if (cls == SG_INV) {
@@ -1702,9 +1719,9 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     } else if (cls == SG_DUP) {
       stp[i] = ST_DUPLICATE;
       nexc += 1;
-      att += ((ks[u] & 0xFFFFu) & gm) + ug;
+      att += ((ks[u] & 0x3FFFu) & gm) + ug;
     } else {
-      defer_push(cls == SG_DEFA ? BA : B, cls == SG_DEFA ? DA : DB, kp[i], vp[i], k0u + i,
+      defer_push(cls == SG_DEFA ? BA : B, cls == SG_DEFA ? DA : DB, kk[u], vp[i], k0u + i,
                  cls == SG_DEFA ? 0u : WINDOW);
       ndef += 1;
     }
