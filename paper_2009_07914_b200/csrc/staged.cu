@@ -95,13 +95,14 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                "l"(src), "r"(bytes), "r"(smem_addr(bar))
                : "memory");
 }
-// shared -> global bulk copy; waits until the writes are performed
+// shared -> global bulk copy; waits until the shared-memory source has been read (the
+// global writes complete on their own before the kernel does)
 __device__ __forceinline__ void bulk_store_wait(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
                "r"(bytes)
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void fence_smem_to_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -1422,26 +1423,17 @@ __device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* wt) {
   return before + x - v;
 }
 
-// x -> min(max(x + p, q), r) on int lags; closed under composition
+// x -> min(max(x + p, q), r) on int lags; closed under composition.  The +-2^24 sentinels
+// stay far from any reachable value (the offsets of one region sum to less than 2^14 in size).
 struct ClampMap {
   int p, q, r;
-  static constexpr int INF = 1 << 30;
+  static constexpr int INF = 1 << 24;
   __device__ __forceinline__ static ClampMap id() { return {0, -INF, INF}; }
-  __device__ __forceinline__ int apply(int x) const {
-    const int y = x + p > q ? x + p : q;
-    return y < r ? y : r;
-  }
+  __device__ __forceinline__ int apply(int x) const { return min(max(x + p, q), r); }
 };
 // g after f
 __device__ __forceinline__ ClampMap compose(const ClampMap& f, const ClampMap& g) {
-  ClampMap h;
-  h.p = f.p + g.p;
-  const int q1 = f.q <= -ClampMap::INF ? -ClampMap::INF : f.q + g.p;
-  h.q = q1 > g.q ? q1 : g.q;
-  const int r1 = f.r >= ClampMap::INF ? ClampMap::INF : f.r + g.p;
-  const int r2 = r1 > g.q ? r1 : g.q;
-  h.r = r2 < g.r ? r2 : g.r;
-  return h;
+  return {f.p + g.p, max(f.q + g.p, g.q), min(max(f.r + g.p, g.q), g.r)};
 }
 // one window-start group: c keys, free indices a = fidx(l), a1 = fidx(l + 1), b = fidx(l + 32)
 __device__ __forceinline__ ClampMap group_map(uint32_t c, uint32_t a, uint32_t a1, uint32_t b) {
@@ -1464,8 +1456,21 @@ __device__ __forceinline__ ClampMap block_excl_clamp(ClampMap x, int (*wsm)[3]) 
   }
   if (lane == 31) wsm[warp][0] = in.p, wsm[warp][1] = in.q, wsm[warp][2] = in.r;
   __syncthreads();
-  ClampMap carry = ClampMap::id();  // the warps before this one
-  for (int w = 0; w < warp; ++w) carry = compose(carry, ClampMap{wsm[w][0], wsm[w][1], wsm[w][2]});
+  // the warps before this one: an exclusive scan of the warp totals, lane w holding warp w's
+  ClampMap wv = lane < NT / 32 ? ClampMap{wsm[lane][0], wsm[lane][1], wsm[lane][2]} : ClampMap::id();
+#pragma unroll
+  for (int d = 1; d < NT / 32; d <<= 1) {
+    ClampMap y;
+    y.p = __shfl_up_sync(0xffffffffu, wv.p, d);
+    y.q = __shfl_up_sync(0xffffffffu, wv.q, d);
+    y.r = __shfl_up_sync(0xffffffffu, wv.r, d);
+    if (lane >= d) wv = compose(y, wv);
+  }
+  ClampMap carry;
+  carry.p = __shfl_sync(0xffffffffu, wv.p, (warp + 31) & 31);
+  carry.q = __shfl_sync(0xffffffffu, wv.q, (warp + 31) & 31);
+  carry.r = __shfl_sync(0xffffffffu, wv.r, (warp + 31) & 31);
+  if (warp == 0) carry = ClampMap::id();
   ClampMap prev;  // the lanes before this one
   prev.p = __shfl_up_sync(0xffffffffu, in.p, 1);
   prev.q = __shfl_up_sync(0xffffffffu, in.q, 1);
@@ -1538,13 +1543,15 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   const uint32_t k0u = (uint32_t)k0;
   uint32_t* const tw = reinterpret_cast<uint32_t*>(tile);
   const uint32_t lane = threadIdx.x & 31u;
-  // the region's keys and window starts (coalesced), in flight while the tile lands
+  // the region's keys and window starts (coalesced), in flight while the tile lands; the
+  // values (needed at the placement) are prefetched into L2
   uint32_t kk[SG_PER], ks0[SG_PER];
 #pragma unroll
   for (int u = 0; u < (int)SG_PER; ++u) {
     const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
     kk[u] = i < m ? __ldcs(kp + i) : 0u;
     ks0[u] = i < m ? (uint32_t)__ldcs(lp + i) : 0u;
+    if (i < m && (threadIdx.x & 31u) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + i));
   }
   __syncthreads();  // zeroed, mbarrier initialised
   mbar_wait(&bar, 0);
@@ -1607,7 +1614,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
         continue;
       }
     }
-    if (fidx(lo) == fidx(lo + WINDOW)) {  // neither the key nor a free cell: resume at window 1
+    if (occ_any && fidx(lo) == fidx(lo + WINDOW)) {  // neither the key nor a free cell: window 1
       ks[u] = SG_DEFB << 28 | lo << 14;
       continue;
     }
@@ -1631,6 +1638,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       const uint32_t l = l0 + (uint32_t)u;
       if (l < ST_R) h = compose(h, group_map(cnt[l], fidx(l), fidx(l + 1), fidx(l + WINDOW)));
     }
+    // (fidx is the identity up to len on an empty tile: the common case costs a min per call)
     int lam = block_excl_clamp<SGT>(h, cm3).apply(0);
 #pragma unroll
     for (int u = 0; u < (int)SG_LPT; ++u) {
@@ -1648,6 +1656,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     }
   }
   __syncthreads();
+  uint32_t nexc = 0, ndef = 0, nsent = 0, occn = 0, att = 0;
   // (d) placement into the staged tile; values load four keys at a time
   auto slot_of = [&](uint32_t fi) -> uint32_t {  // the fi-th free slot
     if (!occ_any) return fi;
@@ -1667,12 +1676,12 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
       const int u = g4 + x;
-      vv[x] = (ks[u] >> 28) == SG_PART ? __ldcs(vp + threadIdx.x + (uint32_t)u * SGT) : 0u;
+      vv[x] = ((ks[u] >> 28) & 7u) == SG_PART ? __ldcs(vp + threadIdx.x + (uint32_t)u * SGT) : 0u;
     }
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
       const int u = g4 + x;
-      if ((ks[u] >> 28) != SG_PART) continue;
+      if (((ks[u] >> 28) & 7u) != SG_PART) continue;
       const uint32_t lo = (ks[u] >> 14) & 0x1FFFu, r = ks[u] & 0x3FFFu;
       if (r >= cnt[lo]) {  // past what window 0 holds for this group: resume at window 1
         ks[u] = SG_DEFB << 28 | 1u << 27 | lo << 14;
@@ -1680,6 +1689,8 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       }
       const uint32_t sl = slot_of((uint32_t)first[lo] + r);
       tile[sl] = (uint64_t)vv[x] << 32 | kk[u];
+      occn += 1;
+      att += ((sl - lo) & gm) + ug;
     }
   }
   __syncthreads();
@@ -1688,7 +1699,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   // pass (nothing has been written to global memory yet).
 #pragma unroll
   for (int u = 0; u < (int)SG_PER; ++u) {
-    const uint32_t cls = ks[u] >> 28;
+    const uint32_t cls = (ks[u] >> 28) & 7u;
     if (cls != SG_PART && !(cls == SG_DEFB && (ks[u] >> 27 & 1u))) continue;
     const uint32_t lo = (ks[u] >> 14) & 0x1FFFu;
     const uint32_t n = cls == SG_PART ? (ks[u] & 0x3FFFu) : cnt[lo];
@@ -1701,17 +1712,13 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     return;
   }
   // (f) results: statuses, deferrals, counters
-  uint32_t nexc = 0, ndef = 0, nsent = 0, occn = 0, att = 0;
 #pragma unroll
   for (int u = 0; u < (int)SG_PER; ++u) {
-    const uint32_t cls = ks[u] >> 28;
+    const uint32_t cls = (ks[u] >> 28) & 7u;
     if (cls == SG_NONE) continue;
     const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
-    const uint32_t lo = (ks[u] >> 14) & 0x1FFFu;
     if (cls == SG_PART) {
-      const uint32_t sl = slot_of((uint32_t)first[lo] + (ks[u] & 0x3FFFu));
-      occn += 1;
-      att += ((sl - lo) & gm) + ug;
+      continue;  // counted at the placement
     } else if (cls == SG_INV) {
       stp[i] = ST_INVALID;
       nexc += 1;
