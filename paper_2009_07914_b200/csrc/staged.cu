@@ -1398,7 +1398,8 @@ constexpr uint32_t SGT = 768;
 constexpr uint32_t SG_MAXK = 9216;            // keys per region (12 per thread)
 constexpr uint32_t SG_PER = SG_MAXK / SGT;    // keys per thread (region order)
 constexpr uint32_t SG_LPT = (ST_R + SGT - 1) / SGT;  // window starts per thread (11)
-constexpr uint32_t SG_DBUF = 256;             // deferrals buffered per region
+constexpr uint32_t SG_DBUF = 192;             // deferrals buffered per region
+constexpr uint32_t SG_CQ = 512;               // duplicate-check queue (~6% of the keys)
 static_assert(SG_MAXK % SGT == 0 && SG_PER <= 12, "sorted pass geometry");
 
 template <int NT>
@@ -1498,7 +1499,10 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   __shared__ DeferBuf<true, SG_DBUF> B;   // -> DB (window full)
   __shared__ DeferBuf<true, SG_DBUF> BA;  // -> DA (window past the region)
   __shared__ uint32_t wt[SGT / 32];
-  __shared__ int s_tomb, s_occ, s_dup;
+  __shared__ int s_tomb, s_dup;
+  __shared__ uint32_t s_qn;
+  __shared__ uint32_t cq_k[SG_CQ];  // duplicate-check queue: key, lo | own rank << 13 (63: not placed)
+  __shared__ uint16_t cq_l[SG_CQ];
   __shared__ int cm3[SGT / 32][3];
   __shared__ __align__(8) uint64_t bar;
   const uint32_t f = blockIdx.x;
@@ -1524,15 +1528,15 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     B.n = 0;
     BA.n = 0;
     s_tomb = 0;
-    s_occ = 0;
     s_dup = 0;
+    s_qn = 0;
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, len * 8u);
     bulk_load(tile, slots + rbase, len * 8u, &bar);
   }
   {
-    uint32_t* z = reinterpret_cast<uint32_t*>(cnt);
-    for (uint32_t w = threadIdx.x; w < ST_R / 2; w += SGT) z[w] = 0;
+    uint32_t* z = reinterpret_cast<uint32_t*>(first);  // first (signatures in (b)) and cnt
+    for (uint32_t w = threadIdx.x; w < ST_R; w += SGT) z[w] = 0;
   }
   const uint32_t e = (uint32_t)T.e, t = (uint32_t)T.t;
   const uint32_t gm = ~((uint32_t)g - 1u), ug = (uint32_t)g;
@@ -1543,6 +1547,15 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   const uint32_t k0u = (uint32_t)k0;
   uint32_t* const tw = reinterpret_cast<uint32_t*>(tile);
   const uint32_t lane = threadIdx.x & 31u;
+  auto cq_push = [&](uint32_t k, uint32_t lo, uint32_t own) {
+    const uint32_t q = atomicAdd(&s_qn, 1u);
+    if (q < SG_CQ) {
+      cq_k[q] = k;
+      cq_l[q] = (uint16_t)(lo | own << 13);
+    } else {
+      s_dup = 1;  // queue full: the concurrent pass takes the region
+    }
+  };
   // the region's keys and window starts (coalesced), in flight while the tile lands; the
   // values (needed at the placement) are prefetched into L2
   uint32_t kk[SG_PER], ks0[SG_PER];
@@ -1555,31 +1568,40 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   }
   __syncthreads();  // zeroed, mbarrier initialised
   mbar_wait(&bar, 0);
-  {  // free-slot bitmap (a warp per 32-slot word); tombstones / occupied cells in the tile
+  // any occupied cell in the tile?  (16-byte reads of the key words; the common case -- a
+  // fresh table -- needs no free-slot bitmap: the free index of slot s is s)
+  bool occ_any;
+  {
+    const uint4* t16 = reinterpret_cast<const uint4*>(tile);
+    bool oc = false;
+    for (uint32_t q = threadIdx.x; q < len / 2; q += SGT) {
+      const uint4 x = t16[q];
+      oc |= (x.x != e) | (x.z != e);
+    }
+    if (len & 1u) oc |= threadIdx.x == 0 && tw[2 * (len - 1)] != e;
+    occ_any = __syncthreads_or(oc) != 0;
+  }
+  if (occ_any) {  // free-slot bitmap (a warp per 32-slot word); tombstones
     for (uint32_t w = threadIdx.x >> 5; w < ST_R / 32; w += SGT / 32) {
       const uint32_t sl = 32 * w + lane;
       const uint32_t kw = sl < len ? tw[2 * sl] : e;
       const uint32_t fb = __ballot_sync(0xffffffffu, sl < len && kw == e);
-      const bool tb = __any_sync(0xffffffffu, sl < len && kw == t), oc = __any_sync(0xffffffffu, kw != e);
+      const bool tb = __any_sync(0xffffffffu, sl < len && kw == t);
       if (lane == 0) {
         freew[w] = fb;
         if (tb) s_tomb = 1;
-        if (oc) s_occ = 1;
       }
     }
-  }
-  __syncthreads();
-  if (s_tomb) {  // tombstones: the deferred-claim rule needs the concurrent pass
-    if (threadIdx.x == 0) redo[f] = 1;
-    return;
-  }
-  const bool occ_any = s_occ != 0;
-  {
+    __syncthreads();
+    if (s_tomb) {  // tombstones: the deferred-claim rule needs the concurrent pass
+      if (threadIdx.x == 0) redo[f] = 1;
+      return;
+    }
     const uint32_t fc = threadIdx.x < ST_R / 32 ? __popc(freew[threadIdx.x]) : 0u;
     const uint32_t fb = block_excl_sum<SGT>(fc, wt);  // syncs
     if (threadIdx.x < ST_R / 32) wpre[threadIdx.x] = (uint16_t)fb;
+    __syncthreads();
   }
-  __syncthreads();
   auto fidx = [&](uint32_t sl) -> uint32_t {  // free slots before slot sl (sl <= ST_R)
     if (!occ_any) return sl < len ? sl : len;  // an empty tile: every staged slot is free
     const uint32_t w = sl >> 5, b = sl & 31u;
@@ -1621,6 +1643,8 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     const uint32_t sh = (lo & 1u) * 16u;
     const uint32_t rk = atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (lo >> 1), 1u << sh) >> sh & 0xFFFFu;
     ks[u] = SG_PART << 28 | lo << 14 | (rk < 0x3FFFu ? rk : 0x3FFFu);
+    const uint32_t bit = 1u << (((k * 0x9E3779B1u) >> 28) + sh);
+    if (atomicOr(reinterpret_cast<uint32_t*>(first) + (lo >> 1), bit) & bit) cq_push(k, lo, rk < 63u ? rk : 63u);
   }
   __syncthreads();
   // (c) the exact greedy over window starts.  With lam_j = (chain end + 1) - a_j, the lag of the
@@ -1685,6 +1709,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       const uint32_t lo = (ks[u] >> 14) & 0x1FFFu, r = ks[u] & 0x3FFFu;
       if (r >= cnt[lo]) {  // past what window 0 holds for this group: resume at window 1
         ks[u] = SG_DEFB << 28 | 1u << 27 | lo << 14;
+        cq_push(kk[u], lo, 63u);  // must not equal a placed key of its group
         continue;
       }
       const uint32_t sl = slot_of((uint32_t)first[lo] + r);
@@ -1694,17 +1719,19 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     }
   }
   __syncthreads();
-  // (e) in-batch duplicates (same key -> same lo): compare with the group's placed keys of lower
-  // rank (an over-placed copy: with all of them).  One found: the region goes to the concurrent
-  // pass (nothing has been written to global memory yet).
-#pragma unroll
-  for (int u = 0; u < (int)SG_PER; ++u) {
-    const uint32_t cls = (ks[u] >> 28) & 7u;
-    if (cls != SG_PART && !(cls == SG_DEFB && (ks[u] >> 27 & 1u))) continue;
-    const uint32_t lo = (ks[u] >> 14) & 0x1FFFu;
-    const uint32_t n = cls == SG_PART ? (ks[u] & 0x3FFFu) : cnt[lo];
-    for (uint32_t x = 0; x < n; ++x)
-      if (tw[2 * slot_of((uint32_t)first[lo] + x)] == kk[u]) s_dup = 1;
+  // (e) in-batch duplicates.  Copies of a key share a window start, so they are in one group.  In
+  // (b) every participant ORs one bit of its key hash into its group's 16-bit signature; a key whose
+  // bit was set already (a copy -- or, for ~6% of the keys, a different key) is queued, as is a
+  // copy that did not fit, and compared here with its group's other placed keys.  One found: the
+  // region goes to the concurrent pass (nothing has been written to global memory yet).
+  {
+    const uint32_t nq = s_qn < SG_CQ ? s_qn : SG_CQ;
+    for (uint32_t q = threadIdx.x; q < nq; q += SGT) {
+      const uint32_t k = cq_k[q], lo = cq_l[q] & 0x1FFFu, own = cq_l[q] >> 13;
+      const uint32_t pl = cnt[lo], f0 = first[lo];
+      for (uint32_t x = 0; x < pl; ++x)
+        if (x != own && tw[2 * slot_of(f0 + x)] == k) s_dup = 1;
+    }
   }
   __syncthreads();
   if (s_dup) {
