@@ -642,3 +642,78 @@ def test_staged_misses_and_erase_vs_direct(rho):
     gone = np.zeros(n, dtype=bool)
     gone[::5] = True
     assert (a[1][:n].astype(bool) == ~gone).all()
+
+
+def _placement_is_valid_linearisation(t):
+    """No erases happened: every live key's window-0 slots before it are occupied (it took the first
+    free cell when it was inserted), and a key stored past window 0 has a full window 0."""
+    from paper_2009_07914_b200.probing import mix64_array
+    k, _, sl = t.for_all_device()
+    k = k.cpu().numpy().view(np.uint32).astype(np.uint64)
+    sl = sl.cpu().numpy().astype(np.int64)
+    c = t.capacity
+    occ = np.zeros(2 * c, dtype=np.int64)
+    occ[sl] = 1
+    occ[sl + c] = 1  # windows wrap around the end of the table
+    pre = np.concatenate([[0], np.cumsum(occ)])
+    h = (mix64_array(k) % np.uint64(c)).astype(np.int64)
+    off = (sl - h) % c
+    span = np.minimum(off, 32)  # slots of window 0 before the key (all of it when past window 0)
+    return bool(((pre[h + span] - pre[h]) == span).all())
+
+
+@pytest.mark.parametrize("rho", [0.9, 0.95])
+def test_sorted_greedy_insert_semantics(rho):
+    """The sorted-greedy region insert (csrc/staged.cu k_st_insert_sg): a fresh table filled by one
+    batch keeps almost every key in window 0 (the greedy's point); later batches into the partly
+    filled table, with in-batch duplicates of several multiplicities (regions holding one are handed
+    to k_st_insert_q), keys already stored and sentinels: one INSERTED per new key with its value
+    stored, DUPLICATE_KEY for the other copies and for stored keys, INVALID_KEY for sentinels, and
+    every placement a valid sequential insert."""
+    n = 1 << 21
+    rng = np.random.default_rng(int(rho * 100) + 11)
+    pool = rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=3 * n, dtype=np.uint64)))
+    cap = int(np.ceil(n / rho))
+    t = SingleValueHashTable(cap, layout="packed", key_bits=32, value_bits=32, group_width=8)
+    t.set_locality("staged")
+    model = {}
+
+    def batch(new, old, ndup):
+        dup = np.concatenate([np.repeat(new[:ndup], 2), np.repeat(new[ndup:ndup + ndup // 8], 5)])
+        keys = np.concatenate([new, dup, old, np.array([(1 << 32) - 1, (1 << 32) - 2], dtype=np.uint64)])
+        keys = keys[rng.permutation(keys.size)]
+        vals = rng.integers(0, 1 << 32, size=keys.size, dtype=np.uint64)
+        st = t.insert_device(keys, vals).cpu().numpy()
+        assert (st[keys >= (1 << 32) - 2] == 3).all()
+        assert (st[np.isin(keys, old)] == 1).all()
+        ins = st == 0
+        ks, cnt = np.unique(keys[ins], return_counts=True)
+        assert (cnt == 1).all() and set(ks.tolist()) == set(new.tolist())
+        assert ((st == 0) | (st == 1) | (st == 3)).all()
+        model.update(zip(keys[ins].tolist(), vals[ins].tolist()))
+        assert t.occupied == len(model)
+
+    def past_window0():
+        from paper_2009_07914_b200.probing import mix64_array
+        k, _, sl = t.for_all_device()
+        h = (mix64_array(k.cpu().numpy().view(np.uint32).astype(np.uint64)) % np.uint64(t.capacity)).astype(np.int64)
+        return ((sl.cpu().numpy() - h) % t.capacity >= 32).mean()
+
+    fresh = pool[: (3 * n) // 4]
+    batch(fresh, np.zeros(0, dtype=np.uint64), 0)  # one fresh batch: empty tiles, sorted placement
+    assert _placement_is_valid_linearisation(t)
+    assert past_window0() < 0.001, past_window0()
+    batch(pool[(3 * n) // 4: (7 * n) // 8], fresh[:50_000], 0)  # partly filled tiles, stored keys
+    assert _placement_is_valid_linearisation(t)
+    batch(pool[(7 * n) // 8: n], fresh[50_000:60_000], 2000)  # + in-batch duplicates
+    assert _placement_is_valid_linearisation(t)
+    q = np.concatenate([np.array(list(model.keys()), dtype=np.uint64), pool[n: n + 100_000]])
+    v, f = t.retrieve_device(q)
+    v = v.cpu().numpy().view(np.uint32).astype(np.uint64)
+    f = f.cpu().numpy().astype(bool)
+    assert f[: len(model)].all() and not f[len(model):].any()
+    assert (v[: len(model)] == np.array(list(model.values()), dtype=np.uint64)).all()
+    t.set_locality("off")  # the direct (COPS) lookups agree
+    dv, df = t.retrieve_device(q)
+    assert (dv.cpu().numpy().view(np.uint32).astype(np.uint64) == v).all()
+    assert (df.cpu().numpy().astype(bool) == f).all()
