@@ -508,16 +508,17 @@ def main() -> None:
         peak, peak_kind = measured_peak()
         ins_gops = n * world / (ins_ms_max * 1e-3) / 1e9
         ret_gops = n * world / (ret_ms_max * 1e-3) / 1e9
-        # dominant kernel: the longer of the insert / retrieve probe kernels, timed with
+        # dominant kernel: the longer of the insert / retrieve region kernels, timed with
         # CUDA events inside the library on the stream they run on (one launch each per op).
         # Algorithmic bytes per launch: staged region passes stream the table
-        # (read + write back for insert) and 11 B per key (key, value, window start, status /
-        # value + found); direct probes touch one 32 B sector per key.
+        # (read + write back for insert) and per key 10 B (insert: key, value, window start;
+        # statuses are pre-set) / 11 B (retrieve: key, window start, value, found); direct
+        # probes touch one 32 B sector per key.
         sched_name = table.batch_schedule(n)
         c = table.capacity
         if sched_name == "staged":
-            cand = [("k_st_probe<0> (staged insert)", k_ins_ms, 16 * c + 11 * n),
-                    ("k_st_probe<1> (staged retrieve)", k_ret_ms, 8 * c + 11 * n)]
+            cand = [("k_st_insert_sg (staged insert)", k_ins_ms, 16 * c + 10 * n),
+                    ("k_st_lookup_q (staged retrieve)", k_ret_ms, 8 * c + 11 * n)]
         else:
             cand = [("k_insert", k_ins_ms, INSERT_BYTES * n), ("k_lookup", k_ret_ms, RETRIEVE_BYTES * n)]
         kname, kms, kbytes_launch = max(cand, key=lambda x: x[1])
