@@ -56,7 +56,7 @@ int loc_unpermute(const Launch& lc, const LocPlan& p, uint64_t n, const uint16_t
 bool staged_supported(const TableRef& T, uint64_t n);
 size_t staged_scratch_bytes(const TableRef& T, uint64_t n, bool insert);
 int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, const void* vals,
-                  uint64_t n, uint8_t* status, void* scratch);
+                  uint64_t n, uint8_t* status, void* scratch, int fresh);
 int staged_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
                   void* vals_out, uint8_t* found, void* scratch);
 size_t mgroup_scratch_bytes(uint64_t n, int kbytes, int vbytes);
@@ -99,6 +99,10 @@ struct ch_table {
   int group_mode = 0;  // multi-value bulk insert: 0 grouped for n >= 4096, 1 per pair
   bool timing = false;
   KernelTimer timer;
+  // ch_clear of a packed table that bulk inserts stage (>= 256 MiB) defers the memset: the next
+  // staged insert starts every region empty and writes every region (staged.cu, fresh); any other
+  // operation performs the clear first (Ordered, ch_read_slot_range).  CH_LAZY_CLEAR=0: always eager.
+  bool pending_clear = false;
 };
 
 namespace {
@@ -129,15 +133,25 @@ struct Ordered {
   Launch lc;
   std::lock_guard<std::mutex> lock;
   DeviceGuard dev;
-  Ordered(ch_table* t_, void* stream) : t(t_), s((cudaStream_t)stream), lock(t_->mu), dev(t_->cfg.device) {
+  int pre = 0;  // a deferred clear that failed to run
+  // lazy_ok: the operation handles a pending clear itself (a staged insert)
+  Ordered(ch_table* t_, void* stream, bool lazy_ok = false)
+      : t(t_), s((cudaStream_t)stream), lock(t_->mu), dev(t_->cfg.device) {
     lc.stream = s;
     lc.device = t->cfg.device;
     lc.sms = t->sms;
     lc.timer = t->timing ? &t->timer : nullptr;
     cudaStreamWaitEvent(s, t->last, 0);
+    if (t->pending_clear && !lazy_ok) {
+      Launch c = lc;
+      c.timer = nullptr;
+      pre = single_clear(c, t->T, t->ts);
+      t->pending_clear = false;
+    }
   }
   int done(int rc) {
     cudaError_t e = cudaEventRecord(t->last, s);
+    if (pre) return pre;
     if (rc) return rc;
     return check(e, "event record");
   }
@@ -411,10 +425,22 @@ int ch_destroy(ch_table* t) {
   return CH_OK;
 }
 
+static bool g_lazy_clear = [] {
+  const char* e = getenv("CH_LAZY_CLEAR");
+  return !(e && e[0] == '0');
+}();
+
 int ch_clear(ch_table* t, void* stream) {
   if (!t) return fail(CH_EINVAL, "null table");
-  Ordered o(t, stream);
-  int rc = single_clear(o.lc, t->T, t->ts);
+  Ordered o(t, stream, true);
+  const bool lazy = g_lazy_clear && t->cfg.kind == CH_SINGLE && t->cfg.layout == CH_PACKED &&
+                    t->T.c * 8ull >= (256ull << 20);
+  int rc = 0;
+  if (lazy) t->pending_clear = true;  // counters reset now, the slots by the next operation
+  else {
+    t->pending_clear = false;
+    rc = single_clear(o.lc, t->T, t->ts);
+  }
   if (!rc) {
     k_zero_counters<<<1, 1, 0, o.s>>>(t->ctr);
     count_launch();
@@ -525,12 +551,15 @@ int ch_insert(ch_table* t, const void* keys, const void* vals, uint64_t n, uint8
   if (!t) return fail(CH_EINVAL, "null table");
   if (t->cfg.kind != CH_SINGLE) return fail(CH_EINVAL, "ch_insert needs a single-value table");
   if (n && (!keys || !vals || !status)) return fail(CH_EINVAL, "null buffer");
-  Ordered o(t, stream);
-  if (use_staged(t, n)) {
+  const bool staged = use_staged(t, n);
+  Ordered o(t, stream, staged);
+  if (staged) {
     Scratch sc(o.s);
     void* p = sc.get(staged_scratch_bytes(t->T, n, true));
     if (!p) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
-    return o.done(staged_insert(o.lc, t->T, t->ts, keys, vals, n, status, p));
+    const int fresh = t->pending_clear ? 1 : 0;
+    t->pending_clear = false;
+    return o.done(staged_insert(o.lc, t->T, t->ts, keys, vals, n, status, p, fresh));
   }
   if (!use_locality(t, n)) return o.done(single_insert(o.lc, t->T, t->ts, keys, vals, n, status, nullptr, 0));
   const LocPlan p = loc_plan(t->T, n, slot_bytes_of(t));
@@ -728,6 +757,15 @@ int ch_read_slot_range(ch_table* t, uint64_t start, uint64_t count, void* h_keys
   std::lock_guard<std::mutex> lock(t->mu);
   DeviceGuard dev(t->cfg.device);
   int rc = check(cudaEventSynchronize(t->last), "synchronize");
+  if (!rc && t->pending_clear) {  // a deferred clear: run it before reading
+    Launch c;
+    c.stream = nullptr;
+    c.device = t->cfg.device;
+    c.sms = t->sms;
+    rc = single_clear(c, t->T, t->ts);
+    if (!rc) rc = check(cudaDeviceSynchronize(), "clear");
+    t->pending_clear = false;
+  }
   if (rc || count == 0) return rc;
   const int kb = t->ts.kbytes, vb = t->ts.vbytes;
   if (t->cfg.layout == CH_SOA) {
@@ -769,6 +807,7 @@ int ch_write_slots(ch_table* t, const void* h_keys, const void* h_vals) {
   DeviceGuard dev(t->cfg.device);
   int rc = check(cudaEventSynchronize(t->last), "synchronize");
   if (rc) return rc;
+  t->pending_clear = false;  // every cell is written below
   const uint64_t c = t->T.c;
   const int kb = t->ts.kbytes, vb = t->ts.vbytes;
   if (t->cfg.layout == CH_SOA) {

@@ -1175,7 +1175,7 @@ __global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, cons
                                                         const uint16_t* __restrict__ los,
                                                         uint8_t* __restrict__ status, DeferOut DA, DeferOut DB, int g,
                                                         unsigned long long* __restrict__ exc,
-                                                        const uint8_t* __restrict__ only) {
+                                                        const uint8_t* __restrict__ only, int fresh) {
   if (only && !only[blockIdx.x]) return;  // after k_st_insert_sg: the regions it handed back
   extern __shared__ __align__(128) unsigned char dsm[];
   uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
@@ -1200,7 +1200,7 @@ __global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, cons
     const uint32_t c2 = P.cur2[f], l2 = P.lim2[f];
     m = c2 < l2 ? c2 : l2;
   }
-  if (m == 0) return;
+  if (m == 0 && !fresh) return;  // (a pending clear still writes the region: fresh)
   const uint64_t rbase = (uint64_t)f << ST_LOG_R;
   const uint32_t len = (uint32_t)((T.c - rbase) < ST_R ? (T.c - rbase) : ST_R);
   uint64_t* slots = static_cast<uint64_t*>(T.slots);
@@ -1210,8 +1210,10 @@ __global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, cons
     s_qn = 0;
     dirty = 0;
     mbar_init(&bar, 1);
-    mbar_expect_tx(&bar, len * 8u);
-    bulk_load(tile, slots + rbase, len * 8u, &bar);
+    if (!fresh) {
+      mbar_expect_tx(&bar, len * 8u);
+      bulk_load(tile, slots + rbase, len * 8u, &bar);
+    }
   }
   const uint32_t e = (uint32_t)T.e, t = (uint32_t)T.t;
   const uint32_t gm = ~((uint32_t)g - 1u), ug = (uint32_t)g;
@@ -1230,7 +1232,13 @@ __global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, cons
     nl = __ldcs(lp + threadIdx.x);
   }
   __syncthreads();  // mbarrier initialised
-  mbar_wait(&bar, 0);
+  if (fresh) {  // the table's clear is pending: the region starts empty
+    for (uint32_t q = threadIdx.x; q < (len + 1) / 2; q += LQT)
+      reinterpret_cast<uint4*>(tile)[q] = make_uint4(e, 0u, e, 0u);
+    __syncthreads();
+  } else {
+    mbar_wait(&bar, 0);
+  }
   {
     const uint32_t words = (len + TILE_PAD + 3) >> 2;
     const uint4* t16 = reinterpret_cast<const uint4*>(tile);
@@ -1360,7 +1368,7 @@ __global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, cons
   }
   defer_flush(B, DB, true);  // syncs
   defer_flush(BA, DA, true);
-  if (occ) dirty = 1;
+  if (occ || fresh) dirty = 1;
   fence_smem_to_async();
   __syncthreads();
   if (threadIdx.x == 0 && dirty) bulk_store_wait(slots + rbase, tile, len * 8u);
@@ -1489,7 +1497,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
                                                          const uint16_t* __restrict__ los,
                                                          uint8_t* __restrict__ status, DeferOut DA, DeferOut DB,
                                                          int g, unsigned long long* __restrict__ exc,
-                                                         uint8_t* __restrict__ redo) {
+                                                         uint8_t* __restrict__ redo, int fresh) {
   extern __shared__ __align__(128) unsigned char dsm[];
   uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
   uint16_t* first = reinterpret_cast<uint16_t*>(tile + ST_R + TILE_PAD);  // per lo: free index of the first key
@@ -1516,7 +1524,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     const uint32_t c2 = P.cur2[f], l2 = P.lim2[f];
     m = c2 < l2 ? c2 : l2;
   }
-  if (m == 0) return;
+  if (m == 0 && !fresh) return;  // (a pending clear still writes the region: fresh)
   if (m > SG_MAXK) {  // skewed region: the concurrent pass takes it
     if (threadIdx.x == 0) redo[f] = 1;
     return;
@@ -1531,8 +1539,10 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     s_dup = 0;
     s_qn = 0;
     mbar_init(&bar, 1);
-    mbar_expect_tx(&bar, len * 8u);
-    bulk_load(tile, slots + rbase, len * 8u, &bar);
+    if (!fresh) {
+      mbar_expect_tx(&bar, len * 8u);
+      bulk_load(tile, slots + rbase, len * 8u, &bar);
+    }
   }
   {
     uint32_t* z = reinterpret_cast<uint32_t*>(first);  // first (signatures in (b)) and cnt
@@ -1567,11 +1577,17 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     if (i < m && (threadIdx.x & 31u) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + i));
   }
   __syncthreads();  // zeroed, mbarrier initialised
-  mbar_wait(&bar, 0);
   // any occupied cell in the tile?  (16-byte reads of the key words; the common case -- a
-  // fresh table -- needs no free-slot bitmap: the free index of slot s is s)
+  // fresh table -- needs no free-slot bitmap: the free index of slot s is s).  With the table's
+  // clear pending (fresh) the region starts empty and is not read at all.
   bool occ_any;
-  {
+  if (fresh) {
+    for (uint32_t q = threadIdx.x; q < (len + 1) / 2; q += SGT)
+      reinterpret_cast<uint4*>(tile)[q] = make_uint4(e, 0u, e, 0u);
+    __syncthreads();
+    occ_any = false;
+  } else {
+    mbar_wait(&bar, 0);
     const uint4* t16 = reinterpret_cast<const uint4*>(tile);
     bool oc = false;
     for (uint32_t q = threadIdx.x; q < len / 2; q += SGT) {
@@ -2091,7 +2107,7 @@ static int st_backward(const Launch& lc, const StPlan& p, const StBufs& b, uint6
 template <int MODE, bool R2>
 static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const Round& r, const uint32_t* pos,
                     uint8_t* status, uint32_t* rv, uint8_t* rf, const DeferOut& DA, const DeferOut& DB, int g,
-                    unsigned long long* exc = nullptr) {
+                    unsigned long long* exc = nullptr, int fresh = 0) {
   cudaEvent_t e0;
   if (MODE == 0 && !R2 && !g_probe_v1) {
     // sorted-greedy placement (k_st_insert_sg), then the uniform-rounds pass (k_st_insert_q)
@@ -2106,7 +2122,7 @@ static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const 
       if ((rc = cuda_check(cudaMemsetAsync(r.redo, 0, p.regions, lc.stream), "memset"))) return rc;
       st_timed(lc, &e0);
       k_st_insert_sg<<<p.regions, SGT, sm2, lc.stream>>>(T, r.part, r.k2, r.v2, r.lo2, status, DA, DB, g, exc,
-                                                         r.redo);
+                                                         r.redo, fresh);
       count_launch();
       st_timed_end(lc, e0);
       if ((rc = cuda_check(cudaGetLastError(), "staged sorted insert"))) return rc;
@@ -2114,7 +2130,8 @@ static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const 
     } else {
       st_timed(lc, &e0);
     }
-    k_st_insert_q<<<p.regions, LQT, sm, lc.stream>>>(T, r.part, r.k2, r.v2, r.lo2, status, DA, DB, g, exc, only);
+    k_st_insert_q<<<p.regions, LQT, sm, lc.stream>>>(T, r.part, r.k2, r.v2, r.lo2, status, DA, DB, g, exc, only,
+                                                     fresh);
     count_launch();
     if (!g_insert_sg) st_timed_end(lc, e0);
     return cuda_check(cudaGetLastError(), "staged region insert");
@@ -2141,8 +2158,15 @@ static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const 
   return cuda_check(cudaGetLastError(), "staged region probe");
 }
 
+// fresh: the table's clear is pending (ch_clear on a staged-size table defers the memset); the
+// region passes then start every region empty and write every region back.
 int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, const void* vals,
-                  uint64_t n, uint8_t* status, void* scratch) {
+                  uint64_t n, uint8_t* status, void* scratch, int fresh) {
+  if (fresh && g_probe_v1) {  // the lane-refill pass reads its regions: clear for real first
+    const int rc = single_clear(lc, T, ts);
+    if (rc) return rc;
+    fresh = 0;
+  }
   const StPlan p = st_plan(T, n);
   size_t total = 0;
   const bool r2 = g_round2;
@@ -2156,7 +2180,7 @@ int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
     rc = st_forward<1>(lc, T, p, b.r1, (const uint32_t*)keys, (const uint32_t*)vals, nullptr, nullptr, n, nullptr, 0,
                        2, &DA);
   if (rc) return rc;
-  if ((rc = st_probe<0, false>(lc, T, p, b.r1, nullptr, b.rf, nullptr, nullptr, DA, DB, ts.g, exc))) return rc;
+  if ((rc = st_probe<0, false>(lc, T, p, b.r1, nullptr, b.rf, nullptr, nullptr, DA, DB, ts.g, exc, fresh))) return rc;
   if (r2) {  // window 1 of the keys whose window 0 was full, staged the same way
     if ((rc = st_forward<2>(lc, T, p, b.r2, b.bk, b.bv, b.bx, nullptr, n, b.dcount + 1, 1, 2))) return rc;
     if ((rc = st_probe<0, true>(lc, T, p, b.r2, b.r2.p2, b.rf, nullptr, nullptr, DA, DA, ts.g, exc))) return rc;
