@@ -717,3 +717,47 @@ def test_sorted_greedy_insert_semantics(rho):
     dv, df = t.retrieve_device(q)
     assert (dv.cpu().numpy().view(np.uint32).astype(np.uint64) == v).all()
     assert (df.cpu().numpy().astype(bool) == f).all()
+
+
+def test_deferred_clear_semantics():
+    """ch_clear of a staged-size packed table defers the memset (api.cu pending_clear): the next
+    staged insert starts every region empty; any other operation -- lookups, a small (direct)
+    insert, slot reads -- sees an empty table."""
+    from paper_2009_07914_b200 import _lib
+    rng = np.random.default_rng(21)
+    pool = rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=1 << 24, dtype=np.uint64)))
+    t = SingleValueHashTable(34_000_000, layout="packed", key_bits=32, value_bits=32, group_width=8)
+    assert t.capacity * 8 >= 256 << 20
+    keys = pool[: 1 << 22]
+    vals = keys ^ np.uint64(0x5A5A5A5A)
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def clear():
+        _lib.check(_lib.lib().ch_clear(t._dt.handle, stream), "clear")
+
+    assert t.batch_schedule(keys.size) == "staged"
+    assert (t.insert_device(keys, vals).cpu().numpy() == 0).all()
+    clear()  # then lookups: nothing found
+    v, f = t.retrieve_device(keys[:100_000])
+    assert not f.cpu().numpy().any() and t.occupied == 0
+    clear()  # then a small direct insert
+    small = pool[-1000:]
+    assert t.batch_schedule(small.size) != "staged"
+    assert (t.insert_device(small, small).cpu().numpy() == 0).all()
+    v, f = t.retrieve_device(np.concatenate([small, keys[:1000]]))
+    f = f.cpu().numpy()
+    assert f[:1000].all() and not f[1000:].any() and t.occupied == 1000
+    clear()  # then slot reads
+    assert t.slots.load_key(0) == (1 << 32) - 1 and t.slots.load_key(t.capacity - 1) == (1 << 32) - 1
+    clear()  # then a staged insert into the pending-clear table, twice in a row
+    for _ in range(2):
+        st = t.insert_device(keys, vals).cpu().numpy()
+        assert (st == 0).all() and t.occupied == keys.size
+        assert _placement_is_valid_linearisation(t)
+        clear()
+    st = t.insert_device(keys[: 1 << 21], vals[: 1 << 21]).cpu().numpy()  # staged (covers c / 16)
+    assert (st == 0).all()
+    v, f = t.retrieve_device(keys)
+    f = f.cpu().numpy()
+    assert f[: 1 << 21].all() and not f[1 << 21:].any()
+    assert (v.cpu().numpy().view(np.uint32)[: 1 << 21] == vals[: 1 << 21].astype(np.uint32)).all()
