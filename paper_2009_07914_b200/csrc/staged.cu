@@ -1637,23 +1637,22 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       ks[u] = SG_INV << 28;
       continue;
     }
-    if (lo + WINDOW > len) {  // window leaves the staged region: COPS kernel from window 0
-      ks[u] = SG_DEFA << 28;
-      continue;
-    }
+    // a window crossing the region end takes part with its own-region slots (they come first in
+    // window order); a key that does not fit there resumes at window 0 in the COPS kernel
+    const uint32_t span = len - lo < WINDOW ? len - lo : WINDOW;
     if (occ_any) {  // stored before the first free cell (single_table.py:198-200)
       uint32_t o = 0;
-      for (; o < WINDOW; ++o) {
+      for (; o < span; ++o) {
         const uint32_t kw = tw[2 * (lo + o)];
         if (kw == e || kw == k) break;
       }
-      if (o < WINDOW && tw[2 * (lo + o)] == k) {
+      if (o < span && tw[2 * (lo + o)] == k) {
         ks[u] = SG_DUP << 28 | lo << 14 | o;
         continue;
       }
     }
-    if (occ_any && fidx(lo) == fidx(lo + WINDOW)) {  // neither the key nor a free cell: window 1
-      ks[u] = SG_DEFB << 28 | lo << 14;
+    if (occ_any && fidx(lo) == fidx(lo + span)) {  // neither the key nor a free cell here
+      ks[u] = (span < WINDOW ? SG_DEFA : SG_DEFB) << 28 | lo << 14;  // the rest of window 0 / window 1
       continue;
     }
     const uint32_t sh = (lo & 1u) * 16u;
@@ -1723,8 +1722,9 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       const int u = g4 + x;
       if (((ks[u] >> 28) & 7u) != SG_PART) continue;
       const uint32_t lo = (ks[u] >> 14) & 0x1FFFu, r = ks[u] & 0x3FFFu;
-      if (r >= cnt[lo]) {  // past what window 0 holds for this group: resume at window 1
-        ks[u] = SG_DEFB << 28 | 1u << 27 | lo << 14;
+      if (r >= cnt[lo]) {  // past what window 0 holds for this group: resume at window 1 (a
+        // window crossing the region end: at window 0, its next-region slots are unexamined)
+        ks[u] = (lo + WINDOW > len ? SG_DEFA : SG_DEFB) << 28 | 1u << 27 | lo << 14;
         cq_push(kk[u], lo, 63u);  // must not equal a placed key of its group
         continue;
       }
