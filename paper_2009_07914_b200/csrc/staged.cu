@@ -69,6 +69,14 @@ __device__ __forceinline__ uint32_t region_of_key(const TableRef& T, uint32_t ke
 
 // ------------------------------------------------------------- TMA helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// shared-memory atomic add as plain PTX (the compiler wraps atomicAdd in its own warp
+// aggregation, ~17 instructions, even where one lane issues it)
+__device__ __forceinline__ uint32_t atom_add_shared(uint32_t* p, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(v) : "memory");
+  return r;
+}
+
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
@@ -519,13 +527,26 @@ __global__ void __launch_bounds__(PT, CH_AB_GATHER_MINB) k_st_gather(uint64_t n,
   // ib: inverse rank | bucket of bucketed slot it * PT + tid << 16.  Lookups (VAL) take the
   // buckets from the split (bid, 1 B per key: 1.03 -> 0.94 ms per level at 2^28); inserts,
   // whose gathers run only after exceptions, rebuild them from the run table (thread b
-  // writes its run's slots).
+  // writes its run's slots).  Full, aligned lookup tiles (vec) write the caller's order four
+  // keys per thread: 16-byte value and 4-byte flag stores, 8-byte inverse-rank loads.
+  const bool vec = VAL && L == 1 && g.cnt == PTILE && ((g.pos0 & 3) == 0) && (((uintptr_t)(dst_v + g.pos0) & 15) == 0) &&
+                   (((uintptr_t)(dst_f + g.pos0) & 3) == 0);
   uint32_t ib[PI];
+  uint2 iv4[PI / 4];
+  if (vec) {
 #pragma unroll
-  for (int it = 0; it < PI; ++it) {  // inverse ranks (and bucket ids) load alongside the run table
-    const uint32_t li = (uint32_t)it * PT + threadIdx.x;
-    ib[it] = li < g.cnt ? (uint32_t)__ldcs(inv + g.pos0 + li) | (VAL ? (uint32_t)__ldcs(bid + g.pos0 + li) << 16 : 0u)
-                        : 0u;
+    for (int h = 0; h < PI / 4; ++h)
+      iv4[h] = __ldcs(reinterpret_cast<const uint2*>(inv + g.pos0) + h * PT + threadIdx.x);
+#pragma unroll
+    for (int it = 0; it < PI; ++it) ib[it] = (uint32_t)__ldcs(bid + g.pos0 + (uint32_t)it * PT + threadIdx.x) << 16;
+  } else {
+#pragma unroll
+    for (int it = 0; it < PI; ++it) {  // inverse ranks (and bucket ids) load alongside the run table
+      const uint32_t li = (uint32_t)it * PT + threadIdx.x;
+      ib[it] = li < g.cnt ? (uint32_t)__ldcs(inv + g.pos0 + li) |
+                                (VAL ? (uint32_t)__ldcs(bid + g.pos0 + li) << 16 : 0u)
+                          : 0u;
+    }
   }
   const uint32_t bo = block_excl_scan(hv, wt);
   gsrc[threadIdx.x] = gs - bo;  // run source minus its tile offset
@@ -557,6 +578,17 @@ __global__ void __launch_bounds__(PT, CH_AB_GATHER_MINB) k_st_gather(uint64_t n,
     }
   }
   __syncthreads();
+  if (vec) {
+#pragma unroll
+    for (int h = 0; h < PI / 4; ++h) {
+      const uint32_t li = 4u * ((uint32_t)h * PT + threadIdx.x);
+      const uint32_t j0 = iv4[h].x & 0xFFFFu, j1 = iv4[h].x >> 16, j2 = iv4[h].y & 0xFFFFu, j3 = iv4[h].y >> 16;
+      *reinterpret_cast<uint4*>(dst_v + g.pos0 + li) = make_uint4(sV[j0], sV[j1], sV[j2], sV[j3]);
+      *reinterpret_cast<uint32_t*>(dst_f + g.pos0 + li) =
+          (uint32_t)sF[j0] | (uint32_t)sF[j1] << 8 | (uint32_t)sF[j2] << 16 | (uint32_t)sF[j3] << 24;
+    }
+    return;
+  }
 #pragma unroll
   for (int it = 0; it < PI; ++it) {
     const uint32_t li = (uint32_t)it * PT + threadIdx.x;
@@ -593,7 +625,7 @@ struct DeferBuf {
 template <bool VALS, uint32_t CAP>
 __device__ __forceinline__ void defer_push(DeferBuf<VALS, CAP>& B, const DeferOut& D, uint32_t k, uint32_t v,
                                            uint32_t x, uint32_t o) {
-  const uint32_t s = atomicAdd(&B.n, 1u);
+  const uint32_t s = atom_add_shared(&B.n, 1u);
   if (s < CAP) {
     B.k[s] = k;
     if (VALS) B.v[s] = v;
@@ -1115,7 +1147,7 @@ __global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, cons
     if (want) {
       const int leader = __ffs(want) - 1;
       uint32_t qb = 0;
-      if ((int)lane == leader) qb = atomicAdd(&s_qn, (uint32_t)__popc(want));
+      if ((int)lane == leader) qb = atom_add_shared(&s_qn, (uint32_t)__popc(want));
       qb = __shfl_sync(0xffffffffu, qb, leader);
       if (open) {
         const uint32_t s = qb + __popc(want & ((1u << lane) - 1u));
@@ -1340,7 +1372,7 @@ __global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, cons
     if (want) {
       const int leader = __ffs(want) - 1;
       uint32_t qb = 0;
-      if ((int)lane == leader) qb = atomicAdd(&s_qn, (uint32_t)__popc(want));
+      if ((int)lane == leader) qb = atom_add_shared(&s_qn, (uint32_t)__popc(want));
       qb = __shfl_sync(0xffffffffu, qb, leader);
       if (open) {
         const uint32_t q = qb + __popc(want & ((1u << lane) - 1u));
@@ -1822,7 +1854,7 @@ static StPlan st_plan(const TableRef& T, uint64_t n) {
   p.tiles2 = p.tiles1 + p.supers;
   p.oa = n < (1ull << 30) && !g_count_mode;
   const double per_region = (double)n * ST_R / (double)T.c;
-  p.cs = p.oa ? (uint32_t)(per_region * (1u << ST_S2) * 1.03) + PTILE : 0u;
+  p.cs = p.oa ? (((uint32_t)(per_region * (1u << ST_S2) * 1.03) + PTILE + 63u) & ~63u) : 0u;  // 64-key aligned
   p.cr = p.oa ? (((uint32_t)(per_region * 1.0625) + 256u + 63u) & ~63u) : 0u;  // regions start on 256 B key lines
   p.n1 = p.oa ? std::max<uint64_t>(n, (uint64_t)p.supers * p.cs) : n;
   p.n2 = p.oa ? (uint64_t)p.regions * p.cr : n;
