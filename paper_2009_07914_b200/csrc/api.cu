@@ -653,7 +653,7 @@ int ch_multi_count(ch_table* t, const void* keys, uint64_t n, uint32_t* counts, 
   Ordered o(t, stream);
   Scratch sc(o.s);
   uint32_t* ll = (uint32_t*)sc.get(n * 4 + 16);
-  unsigned long long* lc2 = (unsigned long long*)sc.get(16);
+  unsigned long long* lc2 = (unsigned long long*)sc.get(multi_scan_counter_bytes());
   if (!ll || !lc2) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
   int rc = multi_scan(o.lc, t->T, t->ts, keys, n, counts, nullptr, nullptr, 0, ll, lc2);
   if (!rc) {
@@ -674,7 +674,7 @@ int ch_multi_retrieve(ch_table* t, const void* keys, uint64_t n, const uint64_t*
   t->host_ops += n;
   Scratch sc(o.s);
   uint32_t* ll = (uint32_t*)sc.get(n * 4 + 16);
-  unsigned long long* lc2 = (unsigned long long*)sc.get(16);
+  unsigned long long* lc2 = (unsigned long long*)sc.get(multi_scan_counter_bytes());
   if (!ll || !lc2) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
   return o.done(multi_scan(o.lc, t->T, t->ts, keys, n, nullptr, offsets, vals_out, 1, ll, lc2));
 }
@@ -688,7 +688,7 @@ int ch_multi_retrieve_slots(ch_table* t, const void* keys, uint64_t n, const uin
   t->host_ops += n;
   Scratch sc(o.s);
   uint32_t* ll = (uint32_t*)sc.get(n * 4 + 16);
-  unsigned long long* lc2 = (unsigned long long*)sc.get(16);
+  unsigned long long* lc2 = (unsigned long long*)sc.get(multi_scan_counter_bytes());
   if (!ll || !lc2) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
   return o.done(multi_scan(o.lc, t->T, t->ts, keys, n, nullptr, offsets, vals_out, 1, ll, lc2, slots_out));
 }

@@ -155,6 +155,10 @@ int single_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
                   int mode);
 int multi_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, const void* vals,
                  uint64_t n, uint8_t* status);
+// multi-value scans: hot chains handed to the CTA walker (multi.cu); the counters scratch of
+// multi_scan holds 4 words and this many 24-byte entries
+constexpr uint64_t kMultiHugeCap = 1ull << 16;
+constexpr size_t multi_scan_counter_bytes() { return 32 + kMultiHugeCap * 24; }
 int multi_scan(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
                uint32_t* counts, const uint64_t* offsets, void* vals_out, int mode, uint32_t* long_list,
                unsigned long long* counters, int64_t* slot_out = nullptr);

@@ -214,6 +214,15 @@ __device__ __forceinline__ V mw_value(const TableRef& T, uint64_t q, uint64_t wo
   else return __ldcg(&static_cast<const CellT<K, V>*>(T.slots)[q].v);
 }
 
+// A chain still open after HUGE_W windows (a Zipf-hot key: ~10^5 copies at s = 0.75 walk
+// ~2.5 * 10^4 windows) is handed to k_multi_walk_cta with its position and running count.
+constexpr uint32_t HUGE_W = 256;
+struct HugeEntry {
+  uint32_t qi, j;              // query, next window index
+  unsigned long long total;    // matches so far
+  unsigned long long ws;       // start slot of window j
+};
+
 template <Layout LAY, typename K, typename V, int MODE>
 __global__ void __launch_bounds__(256) k_multi_walk(TableRef T, const K* __restrict__ keys, uint64_t n,
                                                     uint32_t* __restrict__ counts,
@@ -221,7 +230,9 @@ __global__ void __launch_bounds__(256) k_multi_walk(TableRef T, const K* __restr
                                                     int64_t* __restrict__ slot_out,
                                                     unsigned long long* __restrict__ next, int g,
                                                     const uint32_t* __restrict__ list,
-                                                    const unsigned long long* __restrict__ n_dev) {
+                                                    const unsigned long long* __restrict__ n_dev,
+                                                    HugeEntry* __restrict__ huge,
+                                                    unsigned long long* __restrict__ n_huge, uint64_t huge_cap) {
   if (n_dev) n = *n_dev;
   constexpr int WW = 4;
   const int lane = threadIdx.x & 31;
@@ -303,7 +314,18 @@ __global__ void __launch_bounds__(256) k_multi_walk(TableRef T, const K* __restr
         if (ws >= T.c) ws -= T.c;
       }
       nw = nw * 2 < (uint32_t)WW ? nw * 2 : (uint32_t)WW;  // 1, 2, 4, 4, ... windows per step
+      if (!done && huge && j >= HUGE_W) {  // a hot key: the CTA walker continues it
+        unsigned long long slot = 0;
+        if (lane == 0) slot = atomicAdd(n_huge, 1ull);
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (slot < huge_cap) {
+          if (lane == 0) huge[slot] = HugeEntry{(uint32_t)qi, j, (unsigned long long)total, (unsigned long long)ws};
+          break;
+        }
+        huge = nullptr;  // list full: walk it here
+      }
     }
+    if (!done) continue;  // handed off
     if (lane == 0) {
       if (MODE == 0) counts[qi] = (uint32_t)total;
       att += (long long)attempts;
@@ -311,6 +333,146 @@ __global__ void __launch_bounds__(256) k_multi_walk(TableRef T, const K* __restr
     }
   }
   // ops are accounted per bulk call on the host side (multi_table.py:249,290: ops += n)
+  const long long v[2] = {att, win};
+  long long* const dst[2] = {(long long*)&T.ctr->attempts, (long long*)&T.ctr->windows};
+  cta_add<2>(v, dst);
+}
+
+// K5 / K6 for the hot keys: one CTA per chain, 128 windows per step (16 warps x 8 windows,
+// all loads independent: the window starts h + j step are known up front), a block-wide cut
+// at the first window holding an empty and a scan of the per-window match counts, so the
+// values land in probe order.  The chain of a key with 10^5 copies takes ~200 steps instead
+// of ~6 * 10^3 dependent steps of the warp walker.
+template <Layout LAY, typename K, typename V, int MODE>
+__global__ void __launch_bounds__(512) k_multi_walk_cta(TableRef T, const K* __restrict__ keys,
+                                                        uint32_t* __restrict__ counts,
+                                                        const uint64_t* __restrict__ offsets, V* __restrict__ out,
+                                                        int64_t* __restrict__ slot_out,
+                                                        const HugeEntry* __restrict__ huge,
+                                                        const unsigned long long* __restrict__ n_huge,
+                                                        unsigned long long* __restrict__ grab, int g) {
+  constexpr uint32_t NWARP = 16, WPW = 8, WSTEP = NWARP * WPW;
+  __shared__ uint32_t s_cnt[WSTEP], s_emp[WSTEP], s_pre[WSTEP];
+  __shared__ unsigned long long s_item;
+  __shared__ uint32_t s_cut, s_sum;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t below = (1u << lane) - 1u;
+  const K e = (K)T.e;
+  const uint32_t ug = (uint32_t)g;
+  const unsigned long long nh = *n_huge;
+  long long att = 0, win = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(grab, 1ull);
+    __syncthreads();
+    const unsigned long long item = s_item;
+    __syncthreads();
+    if (item >= nh) break;
+    const HugeEntry he = huge[item];
+    const K k = keys[he.qi];
+    const ProbeStart ps = probe_start(T, (uint64_t)k);
+    uint64_t base = 0, want = ~0ull;
+    if (MODE == 1) {
+      base = offsets[he.qi];
+      want = offsets[he.qi + 1] - base;
+    }
+    uint64_t total = he.total, jb = he.j, wsb = he.ws;
+    for (;;) {  // CTA-uniform
+      // this warp's first window: wsb + (warp WPW) step mod c
+      uint64_t ws = T.modc.mod(wsb + (uint64_t)(warp * WPW) * ps.step);
+      uint64_t words[WPW];
+      uint32_t kms[WPW];
+#pragma unroll
+      for (uint32_t v = 0; v < WPW; ++v) {
+        const uint64_t jj = jb + warp * WPW + v;
+        uint64_t q = ws + lane;
+        if (q >= T.c) q -= T.c;
+        words[v] = jj < T.max_windows ? mw_load<LAY, K, V>(T, q) : 0;
+        ws += ps.step;
+        if (ws >= T.c) ws -= T.c;
+      }
+#pragma unroll
+      for (uint32_t v = 0; v < WPW; ++v) {
+        const uint64_t jj = jb + warp * WPW + v;
+        const K c = (K)words[v];
+        const uint32_t em = __ballot_sync(0xffffffffu, c == e);
+        const uint32_t km = __ballot_sync(0xffffffffu, c == k) & below_lowest(em);
+        kms[v] = km;
+        if (lane == 0) {
+          s_cnt[warp * WPW + v] = __popc(km);
+          // 1 + lowest empty lane; 33: the window budget ends here (probing.py:214-217)
+          s_emp[warp * WPW + v] = jj >= T.max_windows ? 33u : (em ? lowest_bit(em) + 1u : 0u);
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {  // the cut (first window with an empty or past the budget) and the scan
+        uint32_t cut = WSTEP;
+        for (uint32_t x0 = 0; x0 < WSTEP; x0 += 32) {
+          const unsigned hb = __ballot_sync(0xffffffffu, s_emp[x0 + lane] != 0);
+          if (hb) {
+            cut = x0 + __ffs(hb) - 1;
+            break;
+          }
+        }
+        uint32_t run = 0;
+        for (uint32_t x0 = 0; x0 < WSTEP; x0 += 32) {
+          const uint32_t x = x0 + lane;
+          const uint32_t cx = x <= cut && s_emp[x] != 33u ? s_cnt[x] : 0u;
+          uint32_t inc = cx;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+            if ((int)lane >= d) inc += y;
+          }
+          s_pre[x] = run + inc - cx;
+          run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) {
+          s_cut = cut;
+          s_sum = run;
+        }
+      }
+      __syncthreads();
+      const uint32_t cut = s_cut;
+      if (MODE == 1) {
+        uint64_t ws2 = T.modc.mod(wsb + (uint64_t)(warp * WPW) * ps.step);
+#pragma unroll
+        for (uint32_t v = 0; v < WPW; ++v) {
+          const uint32_t x = warp * WPW + v;
+          if (x <= cut && s_emp[x] != 33u && ((kms[v] >> lane) & 1u)) {
+            const uint64_t r = total + s_pre[x] + __popc(kms[v] & below);
+            uint64_t q = ws2 + lane;
+            if (q >= T.c) q -= T.c;
+            if (r < want) {  // racing writer: keep the length (multi_table.py:285-286)
+              out[base + r] = mw_value<LAY, K, V>(T, q, words[v]);
+              if (slot_out) slot_out[base + r] = (int64_t)q;
+            }
+          }
+          ws2 += ps.step;
+          if (ws2 >= T.c) ws2 -= T.c;
+        }
+      }
+      total += s_sum;
+      if (cut < WSTEP) {
+        if (threadIdx.x == 0) {
+          const uint32_t em1 = s_emp[cut];
+          const uint64_t jc = jb + cut;
+          if (em1 == 33u) {
+            att += (long long)(T.max_windows * WINDOW);
+            win += (long long)T.max_windows;
+          } else {
+            att += (long long)(jc * WINDOW + chunk_end(em1 - 1u, ug));
+            win += (long long)(jc + 1);
+          }
+          if (MODE == 0) counts[he.qi] = (uint32_t)total;
+        }
+        __syncthreads();
+        break;
+      }
+      jb += WSTEP;
+      wsb = T.modc.mod(wsb + (uint64_t)WSTEP * ps.step);
+      __syncthreads();
+    }
+  }
   const long long v[2] = {att, win};
   long long* const dst[2] = {(long long*)&T.ctr->attempts, (long long*)&T.ctr->windows};
   cta_add<2>(v, dst);
@@ -325,13 +487,16 @@ struct MultiKernels {
       kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, (const V*)vals, n, status);
     });
   }
-  // thread pass (first kBudget windows), then the warp walker over the queries it handed off
+  // thread pass (first kBudget windows), then the warp walker over the queries it handed off,
+  // then the CTA walker over the chains the warps handed off (counters: [0] long list, [1] warp
+  // grab, [2] hot list, [3] CTA grab, then kHugeCap hot-list entries)
   static constexpr uint32_t kBudget = 4;
+  static constexpr uint64_t kHugeCap = kMultiHugeCap;
   static int scan(const Launch& lc, const TableRef& T, const void* keys, uint64_t n, uint32_t* counts,
                   const uint64_t* offsets, void* out, int mode, uint32_t* long_list,
                   unsigned long long* counters, int64_t* slot_out) {
     if (n == 0) return 0;
-    int rc = cuda_check(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), lc.stream), "memset");
+    int rc = cuda_check(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), lc.stream), "memset");
     if (rc) return rc;
     if (mode == 0) {
       auto kern = k_multi_scan<LAY, K, V, G, 0>;
@@ -348,14 +513,26 @@ struct MultiKernels {
     }
     if (rc) return rc;
     const unsigned grid = (unsigned)(lc.sms * 8);
+    HugeEntry* huge = reinterpret_cast<HugeEntry*>(counters + 4);
     if (mode == 0)
       k_multi_walk<LAY, K, V, 0><<<grid, 256, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out,
-                                                             slot_out, counters + 1, G, long_list, counters);
+                                                             slot_out, counters + 1, G, long_list, counters,
+                                                             huge, counters + 2, kHugeCap);
     else
       k_multi_walk<LAY, K, V, 1><<<grid, 256, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out,
-                                                             slot_out, counters + 1, G, long_list, counters);
+                                                             slot_out, counters + 1, G, long_list, counters,
+                                                             huge, counters + 2, kHugeCap);
     count_launch();
-    return cuda_check(cudaGetLastError(), "multi walk");
+    if ((rc = cuda_check(cudaGetLastError(), "multi walk"))) return rc;
+    const unsigned grid2 = (unsigned)(lc.sms * 2);  // CTAs take hot chains from a counter; most exit at once
+    if (mode == 0)
+      k_multi_walk_cta<LAY, K, V, 0><<<grid2, 512, 0, lc.stream>>>(T, (const K*)keys, counts, offsets, (V*)out,
+                                                                  slot_out, huge, counters + 2, counters + 3, G);
+    else
+      k_multi_walk_cta<LAY, K, V, 1><<<grid2, 512, 0, lc.stream>>>(T, (const K*)keys, counts, offsets, (V*)out,
+                                                                  slot_out, huge, counters + 2, counters + 3, G);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "multi walk (hot chains)");
   }
 };
 

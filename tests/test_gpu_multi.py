@@ -183,3 +183,34 @@ def test_grouped_insert_zipf_matches_pairwise(layout):
         res.append((offsets, flat[o]))
     assert (res[0][0] == res[1][0]).all() and (res[0][1] == res[1][1]).all()
     assert res[0][0][-1] == n
+
+
+def test_hot_chain_cta_walker():
+    """A key with tens of thousands of copies walks far more than HUGE_W windows: the warp walker
+    hands it to the CTA walker (csrc/multi.cu k_multi_walk_cta, 128 windows per step).  Its count
+    is exact and its values come back in probe order (the grouped insert placed copies 1..m in
+    sequence order), next to ordinary keys."""
+    rng = np.random.default_rng(77)
+    m_hot = 60_000
+    hot = np.uint64(123456789)
+    bg = rng.integers(1, (1 << 31) - 3, size=1 << 20, dtype=np.uint64)
+    bg = bg[bg != hot]
+    keys = np.concatenate([np.full(m_hot, hot, dtype=np.uint64), bg])
+    vals = np.concatenate([np.arange(1, m_hot + 1, dtype=np.uint64), rng.integers(0, 1 << 32, size=bg.size,
+                                                                                   dtype=np.uint64)])
+    t = MultiValueHashTable(int(np.ceil(keys.size / 0.8)), layout="packed", key_bits=32, value_bits=32,
+                            group_width=8)
+    st = t.insert_device(keys, vals).cpu().numpy()
+    assert (st == 0).all() and t.occupied == keys.size
+    q = np.concatenate([np.array([hot], dtype=np.uint64), bg[:5000]])
+    offsets, flat = t.retrieve_device(q)
+    offsets = offsets.cpu().numpy()
+    flat = flat.cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert offsets[1] - offsets[0] == m_hot
+    assert (flat[: m_hot] == np.arange(1, m_hot + 1, dtype=np.uint64)).all()  # probe order
+    counts = np.diff(offsets)[1:]
+    u, c = np.unique(bg, return_counts=True)
+    want = dict(zip(u.tolist(), c.tolist()))
+    assert all(int(counts[i]) == want[int(k)] for i, k in enumerate(bg[:5000]))
+    cnt, _ = t.count_device(q)
+    assert int(cnt.cpu().numpy()[0]) == m_hot
