@@ -95,12 +95,186 @@ __device__ __forceinline__ void mg_store_value(const TableRef& T, uint64_t q, V 
 // table is emptiest and no hot key is left as the kernel's tail.
 constexpr uint32_t MG_BIG = 256;
 constexpr uint32_t MG_SMALL = 8;  // groups below this are placed a thread per group (k_mg_small)
+constexpr uint32_t MG_HUGE = 8192;  // groups this large are placed a CTA per group (k_mg_place_cta)
 __global__ void k_mg_big(const uint32_t* __restrict__ gstart, const uint64_t* __restrict__ ngroups_p,
-                         uint32_t* __restrict__ big, unsigned long long* __restrict__ nbig) {
+                         uint32_t* __restrict__ big, unsigned long long* __restrict__ nbig,
+                         uint32_t* __restrict__ huge, unsigned long long* __restrict__ nhuge) {
   const uint64_t ng = *ngroups_p;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += stride)
-    if (gstart[i + 1] - gstart[i] >= MG_BIG) big[atomicAdd(nbig, 1ull)] = (uint32_t)i;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += stride) {
+    const uint32_t m = gstart[i + 1] - gstart[i];
+    if (m >= MG_HUGE) huge[atomicAdd(nhuge, 1ull)] = (uint32_t)i;
+    else if (m >= MG_BIG) big[atomicAdd(nbig, 1ull)] = (uint32_t)i;
+  }
+}
+
+// The hottest groups (>= MG_HUGE copies: a Zipf s = 0.75 batch of 2^27 pairs has keys with
+// ~6 * 10^5) placed one CTA per group, 128 windows per step (16 warps x 8, independent loads:
+// the window starts h + j step are known up front): a block scan of the windows' free cells
+// hands the group's next copies the first free cells in sequence order, every lane claims its
+// cell with CAS, and the values go to the cells won, in sequence order.  A cell lost to another
+// key is occupied afterwards, so the copies still fill the first free cells of the sequence
+// (the reference inserting them one after another, the others' claims linearised first); the
+// next step resumes after the last cell tried.  Runs before k_mg_place, on the emptiest table.
+template <Layout LAY, typename K, typename V, typename P>
+__global__ void __launch_bounds__(512) k_mg_place_cta(TableRef T, const K* __restrict__ sk,
+                                                      const P* __restrict__ sidx,
+                                                      const uint32_t* __restrict__ gstart,
+                                                      const uint32_t* __restrict__ huge,
+                                                      const unsigned long long* __restrict__ nhuge_p,
+                                                      unsigned long long* __restrict__ grab,
+                                                      const V* __restrict__ vals, uint8_t* __restrict__ status, int g) {
+  constexpr uint32_t NWARP = 16, WPW = 8, WSTEP = NWARP * WPW;
+  __shared__ uint32_t s_free[WSTEP], s_pre[WSTEP], s_won[WSTEP], s_wpre[WSTEP];
+  __shared__ uint32_t s_tot, s_wtot, s_lastx, s_lastlane;
+  __shared__ unsigned long long s_item;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t below = (1u << lane) - 1u;
+  const K e = (K)T.e, tomb = (K)T.t;
+  const uint32_t ug = (uint32_t)g;
+  const unsigned long long nh = *nhuge_p;
+  long long ops = 0, att = 0, win = 0, occ = 0;
+  // exclusive scan of x[0..WSTEP) by warp 0 into pre; returns the total (all warp-0 lanes)
+  auto scan128 = [&](const uint32_t* x, uint32_t* pre) -> uint32_t {
+    uint32_t run = 0;
+    for (uint32_t x0 = 0; x0 < WSTEP; x0 += 32) {
+      const uint32_t cx = x[x0 + lane];
+      uint32_t inc = cx;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+        if ((int)lane >= d) inc += y;
+      }
+      pre[x0 + lane] = run + inc - cx;
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    return run;
+  };
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(grab, 1ull);
+    __syncthreads();
+    const unsigned long long item = s_item;
+    __syncthreads();
+    if (item >= nh) break;
+    const uint32_t gi = huge[item];
+    const uint32_t base = gstart[gi], m = gstart[gi + 1] - base;
+    const K k = sk[base];
+    if (k == e || k == tomb) {  // INVALID_KEY, no accounting (multi_table.py:213-215)
+      for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) status[pay_idx(sidx[base + x])] = ST_INVALID;
+      continue;
+    }
+    const ProbeStart ps = probe_start(T, (uint64_t)k);
+    uint64_t jb = 0, wsb = ps.h;
+    uint32_t o = 0, placed = 0;
+    bool exhausted = false;
+    while (placed < m && !exhausted) {  // CTA-uniform
+      const uint32_t need = m - placed;
+      uint64_t ws = T.modc.mod(wsb + (uint64_t)(warp * WPW) * ps.step);
+      K c[WPW];
+      uint32_t fmv[WPW];
+#pragma unroll
+      for (uint32_t v = 0; v < WPW; ++v) {
+        const uint64_t jj = jb + warp * WPW + v;
+        uint64_t q = ws + lane;
+        if (q >= T.c) q -= T.c;
+        c[v] = jj < T.max_windows ? mg_key<LAY, K, V>(T, q) : k;  // past the budget: "not free"
+        ws += ps.step;
+        if (ws >= T.c) ws -= T.c;
+      }
+#pragma unroll
+      for (uint32_t v = 0; v < WPW; ++v) {
+        const uint32_t x = warp * WPW + v;
+        const bool fr = (x > 0 || lane >= o) && (c[v] == e || c[v] == tomb);  // lowest free first
+        fmv[v] = __ballot_sync(0xffffffffu, fr);
+        if (lane == 0) s_free[x] = __popc(fmv[v]);
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t tot = scan128(s_free, s_pre);
+        if (lane == 0) s_tot = tot;
+      }
+      __syncthreads();
+      // the first `need` free cells in sequence order: claim them
+      const uint32_t tot = s_tot, take = need < tot ? need : tot;
+      uint32_t wonv[WPW];
+      ws = T.modc.mod(wsb + (uint64_t)(warp * WPW) * ps.step);
+#pragma unroll
+      for (uint32_t v = 0; v < WPW; ++v) {
+        const uint32_t x = warp * WPW + v;
+        const uint32_t rank = s_pre[x] + __popc(fmv[v] & below);
+        const bool sel = ((fmv[v] >> lane) & 1u) && rank < take;
+        uint64_t q = ws + lane;
+        if (q >= T.c) q -= T.c;
+        const bool won = sel && mg_claim<LAY, K, V>(T, q, c[v], k);
+        wonv[v] = __ballot_sync(0xffffffffu, won);
+        if (lane == 0) s_won[x] = __popc(wonv[v]);
+        if (sel && rank == take - 1) {  // the last cell tried
+          s_lastx = x;
+          s_lastlane = lane;
+        }
+        ws += ps.step;
+        if (ws >= T.c) ws -= T.c;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t wt = scan128(s_won, s_wpre);
+        if (lane == 0) s_wtot = wt;
+      }
+      __syncthreads();
+      // values of the copies, in sequence order of the cells won
+      ws = T.modc.mod(wsb + (uint64_t)(warp * WPW) * ps.step);
+#pragma unroll
+      for (uint32_t v = 0; v < WPW; ++v) {
+        const uint32_t x = warp * WPW + v;
+        if ((wonv[v] >> lane) & 1u) {
+          const uint32_t idx = placed + s_wpre[x] + __popc(wonv[v] & below);
+          const P pv = sidx[base + idx];
+          uint64_t q = ws + lane;
+          if (q >= T.c) q -= T.c;
+          mg_store_value<LAY, K, V>(T, q, sizeof(P) == 8 ? (V)(uint32_t)pv : vals[pay_idx(pv)]);
+          const uint64_t jj = jb + x;
+          att += (long long)(jj * WINDOW + chunk_end(lane, ug));
+          win += (long long)(jj + 1);
+        }
+        ws += ps.step;
+        if (ws >= T.c) ws -= T.c;
+      }
+      placed += s_wtot;
+      // resume after the last cell tried, or after these windows when every free cell was tried
+      if (placed < m) {
+        if (take < tot) {
+          const uint32_t lx = s_lastx, ll = s_lastlane;
+          jb += lx;
+          wsb = T.modc.mod(wsb + (uint64_t)lx * ps.step);
+          o = ll + 1;
+          if (o >= WINDOW) {
+            o = 0;
+            jb += 1;
+            wsb += ps.step;
+            if (wsb >= T.c) wsb -= T.c;
+          }
+        } else {
+          jb += WSTEP;
+          wsb = T.modc.mod(wsb + (uint64_t)WSTEP * ps.step);
+          o = 0;
+        }
+        if (jb >= T.max_windows) exhausted = true;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      ops += m;
+      occ += placed;
+      const uint64_t lost = m - placed;  // sequence exhausted: TABLE_FULL, whole budget walked
+      att += (long long)(lost * (uint64_t)T.max_windows * WINDOW);
+      win += (long long)(lost * T.max_windows);
+    }
+    for (uint32_t x = placed + threadIdx.x; x < m; x += blockDim.x) status[pay_idx(sidx[base + x])] = ST_TABLE_FULL;
+  }
+  const long long v[4] = {ops, att, win, occ};
+  long long* const dst[4] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
+                             &T.ctr->occupied};
+  cta_add<4>(v, dst);
 }
 
 // One warp per distinct key (big groups first, then the rest in sorted order, taken from
@@ -334,7 +508,7 @@ size_t mgroup_scratch_bytes(uint64_t n, int kbytes, int vbytes) {
   const size_t sort_b = kbytes == 8 ? sort_temp_bytes<uint64_t, uint64_t>(n) : sort_temp_bytes<uint32_t, uint64_t>(n);
   (void)vbytes;
   return al256(sort_b) + al256(n * kbytes) + 2 * al256(n * 8) + al256(n * 4) + al256((n + 1) * 8) +
-         al256(exclusive_scan_scratch_bytes(n)) + 2 * al256((n + 1) * 4) + 256;
+         al256(exclusive_scan_scratch_bytes(n)) + 2 * al256((n + 1) * 4) + 256 + al256((n / MG_HUGE + 1) * 4);
 }
 
 template <Layout LAY, typename K, typename V>
@@ -362,13 +536,14 @@ static int mgroup_impl(const Launch& lc, const TableRef& T, int g, const K* keys
   void* scan = take(scan_b);
   uint32_t* gstart = (uint32_t*)take((n + 1) * 4);
   uint32_t* big = (uint32_t*)take((n + 1) * 4);
-  unsigned long long* next = (unsigned long long*)take(64);  // [0] big-group grab, [1] big groups, [2] grab
+  unsigned long long* next = (unsigned long long*)take(64);  // [0] big grab, [1] big groups, [2] grab, [3] huge, [4] huge grab
+  uint32_t* huge = (uint32_t*)take((n / MG_HUGE + 1) * 4);
   if ((size_t)(q - static_cast<char*>(scratch)) > scratch_bytes) {
     set_error("grouped insert scratch too small");
     return -22;
   }
   int rc = cuda_check(cudaMemsetAsync(status, ST_INSERTED, n, lc.stream), "memset");
-  if (!rc) rc = cuda_check(cudaMemsetAsync(next, 0, 24, lc.stream), "memset");  // big grab, nbig, small grab
+  if (!rc) rc = cuda_check(cudaMemsetAsync(next, 0, 40, lc.stream), "memset");  // grabs and list counts
   if (rc) return rc;
   const unsigned grid = (unsigned)(lc.sms * 8);
   k_mg_payload<P, V><<<grid, MG_THREADS, 0, lc.stream>>>(idx, vals, n);
@@ -383,12 +558,15 @@ static int mgroup_impl(const Launch& lc, const TableRef& T, int g, const K* keys
   if ((rc = exclusive_scan_u32(lc, head, n, hoff, scan, scan_b))) return rc;
   k_mg_starts<<<grid, MG_THREADS, 0, lc.stream>>>(head, hoff, n, gstart);
   count_launch();
-  k_mg_big<<<grid, MG_THREADS, 0, lc.stream>>>(gstart, hoff + n, big, next + 1);
+  k_mg_big<<<grid, MG_THREADS, 0, lc.stream>>>(gstart, hoff + n, big, next + 1, huge, next + 3);
   count_launch();
   if ((rc = cuda_check(cudaGetLastError(), "group runs"))) return rc;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (lc.timer && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess)
     cudaEventRecord(e0, lc.stream);
+  k_mg_place_cta<LAY, K, V, P><<<(unsigned)lc.sms, 512, 0, lc.stream>>>(T, sk, sidx, gstart, huge, next + 3, next + 4,
+                                                                        vals, status, g);
+  count_launch();
   k_mg_place<LAY, K, V, P><<<grid, MG_THREADS, 0, lc.stream>>>(T, sk, sidx, gstart, hoff + n, big, next + 1, next,
                                                                 vals, status, g, g_mw);
   count_launch();
