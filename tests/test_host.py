@@ -207,3 +207,26 @@ def test_all_to_all_exchange_gloo_world2():
     res = sorted(q.get(timeout=5) for _ in range(2))
     assert all(ok for _, ok, _ in res)
     assert res[0][2] == 5000 + 5037
+
+
+def test_sorted_greedy_scan_model():
+    """The sorted-greedy region insert's parallel form (csrc/staged.cu k_st_insert_sg: clamped
+    additions composed by one scan over the window starts) equals the sequential greedy slot for
+    slot on random regions with pre-occupied slots, and keeps far more keys in window 0 than an
+    arbitrary claim order (tools/sim_sorted_greedy.py)."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("sim_sg", os.path.join(root, "tools", "sim_sorted_greedy.py"))
+    sim = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(sim)
+    rng = np.random.default_rng(9)
+    for _ in range(4):
+        pre = rng.uniform(0, 0.5)
+        occ = rng.random(sim.R) < pre
+        m = int(sim.R * rng.uniform(0.6, 1.05) * (1 - pre))
+        lo = np.sort(rng.integers(0, sim.R - sim.W + 1, size=m))
+        assert sim.sequential(lo, occ) == sim.clamp_scan(lo, occ)
+    m = int(sim.R * 0.95)
+    lo = rng.integers(0, sim.R - sim.W + 1, size=m)
+    empty = np.zeros(sim.R, bool)
+    assert sim.sequential(np.sort(lo), empty).count(-1) * 5 < sim.sequential(lo, empty).count(-1)
