@@ -1532,9 +1532,10 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
                                                          uint8_t* __restrict__ redo, int fresh) {
   extern __shared__ __align__(128) unsigned char dsm[];
   uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
-  uint16_t* first = reinterpret_cast<uint16_t*>(tile + ST_R + TILE_PAD);  // per lo: free index of the first key
-  uint16_t* cnt = first + ST_R;                                            // per lo: participants -> placed
-  uint32_t* freew = reinterpret_cast<uint32_t*>(cnt + ST_R);               // free-slot bitmap
+  // per window start lo: participants (bits 0..15) | signature of their key hashes (16..31);
+  // after the scan (c): free index of the group's first key (0..15) | keys placed (16..31)
+  uint32_t* cs = reinterpret_cast<uint32_t*>(tile + ST_R + TILE_PAD);
+  uint32_t* freew = cs + ST_R;                                             // free-slot bitmap
   uint16_t* wpre = reinterpret_cast<uint16_t*>(freew + ST_R / 32);         // free slots before word w
   __shared__ DeferBuf<true, SG_DBUF> B;   // -> DB (window full)
   __shared__ DeferBuf<true, SG_DBUF> BA;  // -> DA (window past the region)
@@ -1576,10 +1577,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       bulk_load(tile, slots + rbase, len * 8u, &bar);
     }
   }
-  {
-    uint32_t* z = reinterpret_cast<uint32_t*>(first);  // first (signatures in (b)) and cnt
-    for (uint32_t w = threadIdx.x; w < ST_R; w += SGT) z[w] = 0;
-  }
+  for (uint32_t w = threadIdx.x; w < ST_R; w += SGT) cs[w] = 0;
   const uint32_t e = (uint32_t)T.e, t = (uint32_t)T.t;
   const uint32_t gm = ~((uint32_t)g - 1u), ug = (uint32_t)g;
   const uint32_t* const kp = keys + k0;
@@ -1590,7 +1588,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   uint32_t* const tw = reinterpret_cast<uint32_t*>(tile);
   const uint32_t lane = threadIdx.x & 31u;
   auto cq_push = [&](uint32_t k, uint32_t lo, uint32_t own) {
-    const uint32_t q = atomicAdd(&s_qn, 1u);
+    const uint32_t q = atom_add_shared(&s_qn, 1u);
     if (q < SG_CQ) {
       cq_k[q] = k;
       cq_l[q] = (uint16_t)(lo | own << 13);
@@ -1687,11 +1685,12 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       ks[u] = (span < WINDOW ? SG_DEFA : SG_DEFB) << 28 | lo << 14;  // the rest of window 0 / window 1
       continue;
     }
-    const uint32_t sh = (lo & 1u) * 16u;
-    const uint32_t rk = atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (lo >> 1), 1u << sh) >> sh & 0xFFFFu;
+    // the rank in the group (count, bits 0..15) and one bit of the key's hash ORed into the
+    // group's signature (bits 16..31) of the same word
+    const uint32_t rk = atom_add_shared(cs + lo, 1u) & 0xFFFFu;
+    const uint32_t bit = 1u << (16u + ((k * 0x9E3779B1u) >> 28));
     ks[u] = SG_PART << 28 | lo << 14 | (rk < 0x3FFFu ? rk : 0x3FFFu);
-    const uint32_t bit = 1u << (((k * 0x9E3779B1u) >> 28) + sh);
-    if (atomicOr(reinterpret_cast<uint32_t*>(first) + (lo >> 1), bit) & bit) cq_push(k, lo, rk < 63u ? rk : 63u);
+    if (atomicOr(cs + lo, bit) & bit) cq_push(k, lo, rk < 63u ? rk : 63u);
   }
   __syncthreads();
   // (c) the exact greedy over window starts.  With lam_j = (chain end + 1) - a_j, the lag of the
@@ -1703,25 +1702,41 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   // min(c_j, w_j - max(lam_j, 0)) -- the sequential greedy exactly (tools/sim_sorted_greedy.py).
   {
     const uint32_t l0 = threadIdx.x * SG_LPT;
+    // free index before slot l, after it, and at the window end (identity up to len on an empty tile)
+    auto abw = [&](uint32_t l, uint32_t& a, uint32_t& a1, uint32_t& b) {
+      if (!occ_any) {
+        a = l < len ? l : len;
+        a1 = l + 1 < len ? l + 1 : len;
+        b = l + WINDOW < len ? l + WINDOW : len;
+      } else {
+        a = fidx(l);
+        a1 = fidx(l + 1);
+        b = fidx(l + WINDOW);
+      }
+    };
     ClampMap h = ClampMap::id();
 #pragma unroll
     for (int u = 0; u < (int)SG_LPT; ++u) {
       const uint32_t l = l0 + (uint32_t)u;
-      if (l < ST_R) h = compose(h, group_map(cnt[l], fidx(l), fidx(l + 1), fidx(l + WINDOW)));
+      if (l < ST_R) {
+        uint32_t a, a1, b;
+        abw(l, a, a1, b);
+        h = compose(h, group_map(cs[l] & 0xFFFFu, a, a1, b));
+      }
     }
-    // (fidx is the identity up to len on an empty tile: the common case costs a min per call)
     int lam = block_excl_clamp<SGT>(h, cm3).apply(0);
 #pragma unroll
     for (int u = 0; u < (int)SG_LPT; ++u) {
       const uint32_t l = l0 + (uint32_t)u;
       if (l >= ST_R) break;
-      const uint32_t c = cnt[l];
-      const int a = (int)fidx(l), a1 = (int)fidx(l + 1), b = (int)fidx(l + WINDOW);
+      const uint32_t c = cs[l] & 0xFFFFu;
+      uint32_t a, a1, b;
+      abw(l, a, a1, b);
       if (c) {
         const int lag = lam > 0 ? lam : 0;
-        const int fit = b - a - lag;
-        first[l] = (uint16_t)(a + lag);
-        cnt[l] = (uint16_t)((int)c < fit ? (int)c : (fit > 0 ? fit : 0));
+        const int fit = (int)b - (int)a - lag;
+        const uint32_t placed = (int)c < fit ? c : (fit > 0 ? (uint32_t)fit : 0u);
+        cs[l] = ((uint32_t)((int)a + lag) & 0xFFFFu) | placed << 16;
       }
       lam = group_map(c, a, a1, b).apply(lam);
     }
@@ -1753,14 +1768,14 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     for (int x = 0; x < 4; ++x) {
       const int u = g4 + x;
       if (((ks[u] >> 28) & 7u) != SG_PART) continue;
-      const uint32_t lo = (ks[u] >> 14) & 0x1FFFu, r = ks[u] & 0x3FFFu;
-      if (r >= cnt[lo]) {  // past what window 0 holds for this group: resume at window 1 (a
+      const uint32_t lo = (ks[u] >> 14) & 0x1FFFu, r = ks[u] & 0x3FFFu, w = cs[lo];
+      if (r >= (w >> 16)) {  // past what window 0 holds for this group: resume at window 1 (a
         // window crossing the region end: at window 0, its next-region slots are unexamined)
         ks[u] = (lo + WINDOW > len ? SG_DEFA : SG_DEFB) << 28 | 1u << 27 | lo << 14;
         cq_push(kk[u], lo, 63u);  // must not equal a placed key of its group
         continue;
       }
-      const uint32_t sl = slot_of((uint32_t)first[lo] + r);
+      const uint32_t sl = slot_of((w & 0xFFFFu) + r);
       tile[sl] = (uint64_t)vv[x] << 32 | kk[u];
       occn += 1;
       att += ((sl - lo) & gm) + ug;
@@ -1776,7 +1791,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     const uint32_t nq = s_qn < SG_CQ ? s_qn : SG_CQ;
     for (uint32_t q = threadIdx.x; q < nq; q += SGT) {
       const uint32_t k = cq_k[q], lo = cq_l[q] & 0x1FFFu, own = cq_l[q] >> 13;
-      const uint32_t pl = cnt[lo], f0 = first[lo];
+      const uint32_t pl = cs[lo] >> 16, f0 = cs[lo] & 0xFFFFu;
       for (uint32_t x = 0; x < pl; ++x)
         if (x != own && tw[2 * slot_of(f0 + x)] == k) s_dup = 1;
     }
@@ -1819,7 +1834,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
                              &T.ctr->occupied, (long long*)exc, (long long*)&T.ctr->deferred};
   cta_add<6>(cv6, dst);
 }
-constexpr size_t insert_sg_smem() { return (size_t)(ST_R + TILE_PAD) * 8 + ST_R * 4 + ST_R / 8 + ST_R / 16; }
+constexpr size_t insert_sg_smem() { return (size_t)(ST_R + TILE_PAD) * 8 + ST_R * 4 + ST_R / 8 + ST_R / 16; }  // tile, cs, freew, wpre
 
 template <int MODE, bool R2>
 constexpr size_t probe_smem() {
