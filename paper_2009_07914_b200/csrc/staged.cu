@@ -1063,11 +1063,14 @@ __global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, cons
   uint8_t* const rfp = res_flag + k0;
   const uint32_t k0u = (uint32_t)k0;
   // first round's keys in flight while the tile lands
-  uint32_t nk = e, nl = 0;
-  if (threadIdx.x < m) {
-    nk = __ldcs(kp + threadIdx.x);
-    nl = __ldcs(lp + threadIdx.x);
-  }
+  // two keys per thread and round (i and i + LQT): independent steps, one queue push
+  uint32_t nk[2] = {e, e}, nl[2] = {0, 0};
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+    if (threadIdx.x + x * LQT < m) {
+      nk[x] = __ldcs(kp + threadIdx.x + x * LQT);
+      nl[x] = __ldcs(lp + threadIdx.x + x * LQT);
+    }
   __syncthreads();  // mbarrier initialised
   mbar_wait(&bar, 0);
   {
@@ -1124,40 +1127,51 @@ __global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, cons
     return false;
   };
 
-  for (uint32_t base = 0; base < m; base += LQT) {  // CTA-uniform rounds
-    const uint32_t i = base + threadIdx.x;
-    const uint32_t k = nk, lo = nl;
-    if (i + LQT < m) {  // next round's keys
-      nk = __ldcs(kp + i + LQT);
-      nl = __ldcs(lp + i + LQT);
-    }
-    bool open = false;
-    uint32_t o = 0;
-    if (i < m) {
-      if (k == e || k == t) {  // sentinels are never stored (single_table.py:391-393)
-        rvp[i] = 0;
-        rfp[i] = 0;
-        nsent += 1;
-      } else {
-        open = step(k, fp7(k) * 0x01010101u, lo, i, o);
+  for (uint32_t base = 0; base < m; base += 2 * LQT) {  // CTA-uniform rounds
+    uint32_t k[2], lo[2], o[2] = {0, 0};
+    bool open[2] = {false, false};
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const uint32_t i = base + x * LQT + threadIdx.x;
+      k[x] = nk[x];
+      lo[x] = nl[x];
+      if (i + 2 * LQT < m) {  // next round's keys
+        nk[x] = __ldcs(kp + i + 2 * LQT);
+        nl[x] = __ldcs(lp + i + 2 * LQT);
       }
     }
-    // warp-aggregated push of the open keys
-    const unsigned want = __ballot_sync(0xffffffffu, open);
-    if (want) {
-      const int leader = __ffs(want) - 1;
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const uint32_t i = base + x * LQT + threadIdx.x;
+      if (i < m) {
+        if (k[x] == e || k[x] == t) {  // sentinels are never stored (single_table.py:391-393)
+          rvp[i] = 0;
+          rfp[i] = 0;
+          nsent += 1;
+        } else {
+          open[x] = step(k[x], fp7(k[x]) * 0x01010101u, lo[x], i, o[x]);
+        }
+      }
+    }
+    // warp-aggregated push of the open keys (both of this round's)
+    const unsigned w0 = __ballot_sync(0xffffffffu, open[0]), w1 = __ballot_sync(0xffffffffu, open[1]);
+    if (w0 | w1) {
+      const int leader = __ffs(w0 | w1) - 1;
       uint32_t qb = 0;
-      if ((int)lane == leader) qb = atom_add_shared(&s_qn, (uint32_t)__popc(want));
+      if ((int)lane == leader) qb = atom_add_shared(&s_qn, (uint32_t)(__popc(w0) + __popc(w1)));
       qb = __shfl_sync(0xffffffffu, qb, leader);
-      if (open) {
-        const uint32_t s = qb + __popc(want & ((1u << lane) - 1u));
-        if (s < LQ_CAP) {
-          qk[s] = k;
-          qi[s] = i;
-          qlo[s] = lo | o << 16;
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        if (!open[x]) continue;
+        const uint32_t i = base + x * LQT + threadIdx.x;
+        const uint32_t sq = qb + (x ? __popc(w0) : 0u) + __popc((x ? w1 : w0) & ((1u << lane) - 1u));
+        if (sq < LQ_CAP) {
+          qk[sq] = k[x];
+          qi[sq] = i;
+          qlo[sq] = lo[x] | o[x] << 16;
         } else {  // queue full (skewed region): finish here
-          const uint32_t rep = fp7(k) * 0x01010101u;
-          while (step(k, rep, lo, i, o)) {
+          const uint32_t rep = fp7(k[x]) * 0x01010101u;
+          while (step(k[x], rep, lo[x], i, o[x])) {
           }
         }
       }
