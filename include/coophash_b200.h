@@ -250,6 +250,14 @@ int ch_multi_split32(const void* d_keys, int key_bytes, const void* d_vals, int 
 int ch_route_split32(const void* d_keys, int key_bytes, const void* d_vals, int val_bytes, uint64_t n,
                      uint32_t shards, uint32_t* d_pos, uint64_t* d_offsets, void* d_keys_out, void* d_vals_out,
                      int device, void* stream);
+/* one-pass route partition (the hash-partitioned table's split; replaces the stable
+ * ch_route_split32 where the order inside a destination does not matter): segment d of
+ * d_keys_out / d_vals_out is [d cap, d cap + d_counts[d]); d_pos[i] = the position of source
+ * element i; *d_flag != 0 when a segment passed cap (the outputs are then invalid).  32-bit
+ * keys and values, shards <= 64, shards * cap < 2^32. */
+int ch_route_part32(const uint32_t* d_keys, const uint32_t* d_vals, uint64_t n, uint32_t shards, uint64_t cap,
+                    uint32_t* d_pos, uint64_t* d_counts, uint32_t* d_keys_out, uint32_t* d_vals_out, int* d_flag,
+                    int device, void* stream);
 int ch_scatter32(const void* d_src, int elem_bytes, const uint32_t* d_perm, uint64_t n, void* d_dst, int device,
                  void* stream);
 int ch_gather32(const void* d_src, int elem_bytes, const uint32_t* d_perm, uint64_t n, void* d_dst, int device,

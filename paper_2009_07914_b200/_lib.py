@@ -97,6 +97,7 @@ _SIGS = {
                                    C.c_int, _P]),
     "ch_scatter32": (C.c_int, [_P, C.c_int, _P, _U64, _P, C.c_int, _P]),
     "ch_route_split32": (C.c_int, [_P, C.c_int, _P, C.c_int, _U64, C.c_uint32, _P, _P, _P, _P, C.c_int, _P]),
+    "ch_route_part32": (C.c_int, [_P, _P, _U64, C.c_uint32, _U64, _P, _P, _P, _P, _P, C.c_int, _P]),
     "ch_gather32": (C.c_int, [_P, C.c_int, _P, _U64, _P, C.c_int, _P]),
 }
 

@@ -26,6 +26,9 @@ void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxe
 
 // prims.cu / bucket.cu entry points
 int mix64_array(const Launch& lc, const uint64_t* in, uint64_t n, uint64_t seed, uint64_t* out);
+int route_part32(const Launch& lc, const uint32_t* keys, const uint32_t* vals, uint64_t n, uint32_t shards,
+                 uint64_t cap, uint32_t* pos, unsigned long long* counts, uint32_t* keys_out, uint32_t* vals_out,
+                 int* flag);
 int multi_split(const Launch& lc, const void* keys, int kbytes, const void* vals, int vbytes, uint64_t n,
                 uint32_t shards, void* perm, int perm_bytes, uint64_t* offsets, void* keys_out, void* vals_out,
                 void* scratch, size_t scratch_bytes);
@@ -945,6 +948,18 @@ int ch_route_split32(const void* keys, int key_bytes, const void* vals, int val_
   if (!p) return fail(CH_ENOMEM, "scratch allocation failed");
   return multi_split(lc, keys, key_bytes, vals, vals ? val_bytes : 4, n, shards, pos, -4, offsets, keys_out,
                      vals_out, p, sb);
+}
+
+int ch_route_part32(const uint32_t* keys, const uint32_t* vals, uint64_t n, uint32_t shards, uint64_t cap,
+                    uint32_t* pos, uint64_t* counts, uint32_t* keys_out, uint32_t* vals_out, int* flag, int device,
+                    void* stream) {
+  if (!counts || !flag || (n && (!keys || !pos || !keys_out))) return fail(CH_EINVAL, "null buffer");
+  if (vals && !vals_out) return fail(CH_EINVAL, "null buffer");
+  if (n >= (1ull << 32) || (uint64_t)shards * cap >= (1ull << 32)) return fail(CH_EINVAL, "positions must fit 32 bits");
+  DeviceGuard dev(device);
+  Launch lc = plain_launch(device, stream);
+  return route_part32(lc, keys, vals, n, shards, cap, pos, reinterpret_cast<unsigned long long*>(counts), keys_out,
+                      vals_out, flag);
 }
 
 int ch_scatter32(const void* src, int elem_bytes, const uint32_t* perm, uint64_t n, void* dst, int device,

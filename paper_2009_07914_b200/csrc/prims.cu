@@ -286,6 +286,112 @@ static int split_impl(const Launch& lc, const K* keys, const V* vals, uint64_t n
   return cuda_check(cudaGetLastError(), "split offsets");
 }
 
+// One-pass route partition (ShardedTable's split, ch_route_part32): a 4096-key tile is
+// bucketed by destination shard in shared memory and written as one run per shard at a
+// cursor inside that shard's fixed-capacity segment [d cap, d cap + count_d) -- no count
+// pass, one read of the batch.  pos[i] = the element's position (the inverse map the results
+// return through).  The order inside a segment is not the input order (the table does not
+// need it); a segment past its capacity raises *flag and the caller takes the stable split.
+constexpr int RP_T = 512, RP_I = 8;
+constexpr uint32_t RP_TILE = (uint32_t)RP_T * RP_I;
+constexpr uint32_t RP_MAX_SHARDS = 64;
+
+template <bool VALS>
+__global__ void __launch_bounds__(RP_T) k_route_part(const uint32_t* __restrict__ keys,
+                                                    const uint32_t* __restrict__ vals, uint64_t n, uint32_t shards,
+                                                    uint64_t cap, uint32_t* __restrict__ pos,
+                                                    unsigned long long* __restrict__ cnt,
+                                                    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                    int* __restrict__ flag) {
+  __shared__ uint32_t sK[RP_TILE];
+  __shared__ uint32_t sV[VALS ? RP_TILE : 1];
+  __shared__ uint8_t sD[RP_TILE];
+  __shared__ uint32_t hist[RP_MAX_SHARDS], boff[RP_MAX_SHARDS];
+  __shared__ unsigned long long gb[RP_MAX_SHARDS];
+  __shared__ uint8_t ovf[RP_MAX_SHARDS];
+  const uint64_t pos0 = (uint64_t)blockIdx.x * RP_TILE;
+  const uint32_t cntt = (uint32_t)((n - pos0) < RP_TILE ? (n - pos0) : RP_TILE);
+  if (threadIdx.x < shards) hist[threadIdx.x] = 0;
+  uint32_t k[RP_I], v[RP_I], d[RP_I];
+#pragma unroll
+  for (int it = 0; it < RP_I; ++it) {
+    const uint32_t li = (uint32_t)it * RP_T + threadIdx.x;
+    k[it] = li < cntt ? __ldcs(keys + pos0 + li) : 0u;
+    if (VALS) v[it] = li < cntt ? __ldcs(vals + pos0 + li) : 0u;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < RP_I; ++it) {
+    const uint32_t li = (uint32_t)it * RP_T + threadIdx.x;
+    if (li >= cntt) continue;
+    const uint32_t dd = route(k[it], shards);  // ShardRouter.route (distributed.py:44-45)
+    d[it] = dd | atomicAdd(&hist[dd], 1u) << 8;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // shard runs: global cursor, tile offset
+    uint32_t run = 0;
+    for (uint32_t b0 = 0; b0 < shards; b0 += 32) {
+      const uint32_t b = b0 + threadIdx.x;
+      const uint32_t hv = b < shards ? hist[b] : 0u;
+      uint32_t inc = hv;
+#pragma unroll
+      for (int dl = 1; dl < 32; dl <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, dl);
+        if ((int)threadIdx.x >= dl) inc += y;
+      }
+      if (b < shards) {
+        boff[b] = run + inc - hv;
+        const unsigned long long old = hv ? atomicAdd(cnt + b, (unsigned long long)hv) : 0ull;
+        gb[b] = (unsigned long long)b * cap + old;
+        ovf[b] = (uint8_t)(old + hv > cap);
+        if (old + hv > cap) *flag = 1;
+      }
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < RP_I; ++it) {
+    const uint32_t li = (uint32_t)it * RP_T + threadIdx.x;
+    if (li >= cntt) continue;
+    const uint32_t dd = d[it] & 0xFFu, r = d[it] >> 8;
+    const uint32_t j = boff[dd] + r;
+    sK[j] = k[it];
+    if (VALS) sV[j] = v[it];
+    sD[j] = (uint8_t)dd;
+    pos[pos0 + li] = (uint32_t)(gb[dd] + r);
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < cntt; j += RP_T) {  // runs, coalesced
+    const uint32_t dd = sD[j];
+    if (ovf[dd]) continue;
+    const unsigned long long dst = gb[dd] + (j - boff[dd]);
+    kout[dst] = sK[j];
+    if (VALS) vout[dst] = sV[j];
+  }
+}
+
+int route_part32(const Launch& lc, const uint32_t* keys, const uint32_t* vals, uint64_t n, uint32_t shards,
+                 uint64_t cap, uint32_t* pos, unsigned long long* counts, uint32_t* keys_out, uint32_t* vals_out,
+                 int* flag) {
+  if (shards < 1 || shards > RP_MAX_SHARDS) {
+    set_error("route partition: 1 to 64 shards");
+    return -22;
+  }
+  int rc = cuda_check(cudaMemsetAsync(counts, 0, shards * sizeof(unsigned long long), lc.stream), "memset");
+  if (!rc) rc = cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), lc.stream), "memset");
+  if (rc || n == 0) return rc;
+  const unsigned tiles = (unsigned)((n + RP_TILE - 1) / RP_TILE);
+  if (vals)
+    k_route_part<true><<<tiles, RP_T, 0, lc.stream>>>(keys, vals, n, shards, cap, pos, counts, keys_out, vals_out,
+                                                       flag);
+  else
+    k_route_part<false><<<tiles, RP_T, 0, lc.stream>>>(keys, nullptr, n, shards, cap, pos, counts, keys_out, nullptr,
+                                                        flag);
+  count_launch();
+  return cuda_check(cudaGetLastError(), "route partition");
+}
+
 int multi_split(const Launch& lc, const void* keys, int kbytes, const void* vals, int vbytes, uint64_t n,
                 uint32_t shards, void* perm, int perm_bytes, uint64_t* offsets, void* keys_out, void* vals_out,
                 void* scratch, size_t scratch_bytes) {

@@ -119,6 +119,27 @@ def route_split_device32(keys: torch.Tensor, num_shards: int, values: torch.Tens
     return pos, offsets, kout, vout
 
 
+def route_part_device32(keys: torch.Tensor, num_shards: int, values: torch.Tensor | None = None, stream=None,
+                        slack: float = 1.05):
+    """One-pass route partition (ch_route_part32) into fixed-capacity segments: segment d is
+    [d cap, d cap + counts[d]) of the outputs, pos[i] the position of element i.  Returns
+    (pos, counts (device u64), flag (device int: a segment passed cap), cap, kout, vout).
+    32-bit keys / values, num_shards <= 64."""
+    dev = keys.device.index
+    n = keys.numel()
+    cap = int(n / num_shards * slack) + 4096
+    pos = torch.empty(n, dtype=torch.int32, device=keys.device)
+    counts = torch.empty(num_shards, dtype=torch.int64, device=keys.device)
+    flag = torch.empty(1, dtype=torch.int32, device=keys.device)
+    kout = torch.empty(num_shards * cap, dtype=keys.dtype, device=keys.device)
+    vout = torch.empty(num_shards * cap, dtype=values.dtype, device=keys.device) if values is not None else None
+    _lib.check(_lib.lib().ch_route_part32(
+        keys.data_ptr(), values.data_ptr() if values is not None else None, n, num_shards, cap, pos.data_ptr(),
+        counts.data_ptr(), kout.data_ptr(), vout.data_ptr() if vout is not None else None, flag.data_ptr(), dev,
+        _io.stream_of(dev, stream)), "route_part32")
+    return pos, counts, flag, cap, kout, vout
+
+
 def gather_device32(src: torch.Tensor, pos: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
     """out[i] = src[pos[i]] (ch_gather32)."""
     dev = src.device.index
@@ -510,7 +531,8 @@ def all_to_all_back(send: torch.Tensor, counts_in: list[int], counts_out: list[i
 
 
 def exchange_segments(sends: Sequence[torch.Tensor], send_counts: list[int], recv_counts: list[int],
-                      group=None) -> list[torch.Tensor]:
+                      group=None, send_starts: list[int] | None = None, recv_starts: list[int] | None = None,
+                      recv_len: int | None = None) -> list[torch.Tensor]:
     """Variable-length all-to-all of several parallel arrays in ONE grouped exchange.
 
     ``sends[j]`` holds segments for ranks 0..W-1 back to back (``send_counts``); the
@@ -524,25 +546,30 @@ def exchange_segments(sends: Sequence[torch.Tensor], send_counts: list[int], rec
     staged = any(_host_staged(t, group) for t in sends)
     home = sends[0].device if sends else None
     src = [t.cpu() if staged else t for t in sends]
-    recvs = [torch.empty(sum(recv_counts), dtype=t.dtype, device=t.device) for t in src]
-    so = [0]
-    for c in send_counts:
-        so.append(so[-1] + c)
-    ro = [0]
-    for c in recv_counts:
-        ro.append(ro[-1] + c)
+    recvs = [torch.empty(recv_len if recv_len is not None else sum(recv_counts), dtype=t.dtype, device=t.device)
+             for t in src]
+    # segment p: [so[p], so[p] + send_counts[p]) / [ro[p], ro[p] + recv_counts[p]); back to back
+    # unless explicit starts are given (fixed-capacity segments of ch_route_part32)
+    so = list(send_starts) if send_starts is not None else [sum(send_counts[:p]) for p in range(world)]
+    ro = list(recv_starts) if recv_starts is not None else [sum(recv_counts[:p]) for p in range(world)]
+    so.append(0)
+    ro.append(0)
+    sc = list(send_counts)
+    rcn = list(recv_counts)
     ops = []
     for j, t in enumerate(src):
         for peer in range(world):
             gpeer = dist.get_global_rank(group, peer) if group is not None else peer
+            s_lo, s_hi = so[peer], so[peer] + sc[peer]
+            r_lo, r_hi = ro[peer], ro[peer] + rcn[peer]
             if peer == rank:
-                if send_counts[peer]:
-                    recvs[j][ro[peer]:ro[peer + 1]].copy_(t[so[peer]:so[peer + 1]])
+                if sc[peer]:
+                    recvs[j][r_lo:r_hi].copy_(t[s_lo:s_hi])
                 continue
-            if send_counts[peer]:
-                ops.append(dist.P2POp(dist.isend, t[so[peer]:so[peer + 1]], gpeer, group))
-            if recv_counts[peer]:
-                ops.append(dist.P2POp(dist.irecv, recvs[j][ro[peer]:ro[peer + 1]], gpeer, group))
+            if sc[peer]:
+                ops.append(dist.P2POp(dist.isend, t[s_lo:s_hi], gpeer, group))
+            if rcn[peer]:
+                ops.append(dist.P2POp(dist.irecv, recvs[j][r_lo:r_hi], gpeer, group))
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()
@@ -555,8 +582,10 @@ class ShardedTable:
     insert_device / retrieve_device are collective: every rank calls them with its own
     batch (distributed.py:131-178, one process per GPU).  Pipeline per call:
 
-      split      route + stable split, u32 split position per source element (K10, ch_route_split32)
-      counts     one all_to_all of the S segment sizes (the only host synchronisation)
+      split      one-pass route partition into fixed-capacity segments, u32 position per source
+                 element (ch_route_part32; the stable ch_route_split32 for 64-bit keys / values,
+                 > 64 ranks or a skewed batch that overflows a segment)
+      counts     one all_to_all of the S segment sizes + the overflow flag (the only host sync)
       exchange   keys (+ values) in ONE grouped send/recv (exchange_segments, NVLink)
       local      the shard's own insert / retrieve (staged regions for full-size batches)
       back       statuses / (values, found) in one grouped exchange
@@ -584,26 +613,53 @@ class ShardedTable:
         both = torch.cat([sc, rc]).cpu().tolist()   # one device -> host read per call
         return both[:self.world], both[self.world:]
 
+    def _split(self, k: torch.Tensor, v: torch.Tensor | None):
+        """Route + split: the one-pass partition into fixed-capacity segments (ch_route_part32)
+        for 32-bit keys / values and <= 64 ranks, the stable split (ch_route_split32)
+        otherwise or when a segment overflowed (skewed batch).  Returns (pos, kout, vout,
+        send counts, recv counts, send starts)."""
+        import torch.distributed as dist
+        if k.element_size() == 4 and (v is None or v.element_size() == 4) and self.world <= 64 and k.numel():
+            pos, cnt, flag, cap, kout, vout = route_part_device32(k, self.world, v)
+            rc = torch.empty_like(cnt)
+            if _host_staged(cnt, self.group):
+                sc_h, rc_h = cnt.cpu(), torch.empty(self.world, dtype=torch.int64)
+                dist.all_to_all_single(rc_h, sc_h, group=self.group)
+                both = torch.cat([sc_h, rc_h, flag.cpu().to(torch.int64)]).tolist()
+            else:
+                dist.all_to_all_single(rc, cnt, group=self.group)
+                both = torch.cat([cnt, rc, flag.to(torch.int64)]).cpu().tolist()  # one device -> host read
+            ovf = torch.tensor([both[-1]], dtype=torch.int64)
+            if not _host_staged(cnt, self.group):
+                ovf = ovf.to(k.device)
+            dist.all_reduce(ovf, group=self.group)  # every rank takes the same path
+            if int(ovf.item()) == 0:
+                return pos, kout, vout, both[:self.world], both[self.world:2 * self.world], \
+                    [p * cap for p in range(self.world)]
+        pos, offsets, kout, vout = route_split_device32(k, self.world, v)
+        send, recv = self._counts(offsets)
+        return pos, kout, vout, send, recv, None
+
     def insert_device(self, keys: torch.Tensor, values: torch.Tensor) -> torch.Tensor:
         k = self.table._keys(keys)
         v = self.table._vals(values)
         if k.numel() != v.numel():
             raise ValueError("keys and values differ in length")
-        pos, offsets, kout, vout = route_split_device32(k, self.world, v)
-        send, recv = self._counts(offsets)
-        rk, rv = exchange_segments([kout, vout], send, recv, self.group)
+        pos, kout, vout, send, recv, starts = self._split(k, v)
+        rk, rv = exchange_segments([kout, vout], send, recv, self.group, send_starts=starts)
         st = self.table.insert_device(rk, rv)
-        (back,) = exchange_segments([st], recv, send, self.group)
+        (back,) = exchange_segments([st], recv, send, self.group, recv_starts=starts,
+                                    recv_len=kout.numel() if starts is not None else None)
         out = torch.empty(k.numel(), dtype=torch.uint8, device=k.device)
         return gather_device32(back, pos, out) if k.numel() else out
 
     def retrieve_device(self, keys: torch.Tensor):
         k = self.table._keys(keys)
-        pos, offsets, kout, _ = route_split_device32(k, self.world)
-        send, recv = self._counts(offsets)
-        (rk,) = exchange_segments([kout], send, recv, self.group)
+        pos, kout, _, send, recv, starts = self._split(k, None)
+        (rk,) = exchange_segments([kout], send, recv, self.group, send_starts=starts)
         v, f = self.table.retrieve_device(rk)
-        vb, fb = exchange_segments([v, f], recv, send, self.group)
+        vb, fb = exchange_segments([v, f], recv, send, self.group, recv_starts=starts,
+                                   recv_len=kout.numel() if starts is not None else None)
         n = k.numel()
         vals = torch.empty(n, dtype=v.dtype, device=k.device)
         found = torch.empty(n, dtype=torch.uint8, device=k.device)

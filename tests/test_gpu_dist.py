@@ -310,3 +310,34 @@ def test_route_split32_inverse_and_gather(shards):
     assert (kout.cpu().numpy().view(np.uint32) == keys[rperm]).all()
     back = gather_device32(vout, pos, torch.empty_like(v))
     assert (back.cpu().numpy().view(np.uint32) == vals).all()
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3, 8, 37, 64])
+def test_route_partition_one_pass(shards):
+    """ch_route_part32 (ShardedTable's split): every element lands in its shard's fixed-capacity
+    segment [d cap, d cap + counts[d]) at pos[i] with its value, counts are exact, and a batch
+    that overflows a segment raises the flag."""
+    from paper_2009_07914_b200.distributed import route_part_device32
+    from paper_2009_07914_b200.probing import mix64_array
+    rng = np.random.default_rng(shards)
+    n = (1 << 20) + 333
+    keys = rng.integers(1, (1 << 32) - 3, size=n, dtype=np.uint64)
+    vals = rng.integers(0, 1 << 32, size=n, dtype=np.uint64)
+    dk = torch.from_numpy(keys.astype(np.uint32).view(np.int32)).cuda()
+    dv = torch.from_numpy(vals.astype(np.uint32).view(np.int32)).cuda()
+    pos, cnt, flag, cap, kout, vout = route_part_device32(dk, shards, dv)
+    assert int(flag.item()) == 0
+    pos = pos.cpu().numpy().view(np.uint32).astype(np.int64)
+    cnt = cnt.cpu().numpy()
+    kout = kout.cpu().numpy().view(np.uint32)
+    vout = vout.cpu().numpy().view(np.uint32)
+    dest = ((mix64_array(keys) >> np.uint64(32)) % np.uint64(shards)).astype(np.int64)
+    assert (cnt == np.bincount(dest, minlength=shards)).all()
+    assert (pos // cap == dest).all() and (pos % cap < cnt[dest]).all()
+    assert np.unique(pos).size == n
+    assert (kout[pos] == keys.astype(np.uint32)).all() and (vout[pos] == vals.astype(np.uint32)).all()
+    if shards > 1:  # every key to shard 0: past its capacity
+        hot = keys[dest == 0][: 40_000]
+        _, _, flag2, _, _, _ = route_part_device32(torch.from_numpy(np.resize(hot, n).astype(np.uint32).view(np.int32))
+                                                   .cuda(), shards)
+        assert int(flag2.item()) == 1

@@ -1,5 +1,5 @@
-"""Per-phase device times (split = route + stable split with the inverse map, back-map =
-coalesced gathers) of the hash-partitioned path at the headline size on ONE B200
+"""Per-phase device times (split = the one-pass route partition ShardedTable uses, beside the
+stable split with the inverse map; back-map = coalesced gathers) of the hash-partitioned path at the headline size on ONE B200
 (2^28 keys per rank, S = 8 destinations): the route + split of the insert batch (keys +
 values) and of the retrieve batch, the inverse-permutation scatters of the results, and the
 local insert / retrieve of a full 2^28 batch -- the inputs to the weak-scaling model in
@@ -51,8 +51,24 @@ def split(with_vals):
                                            vo.data_ptr() if with_vals else None, 0, strm()))
 
 
-res["split_insert_ms"], _ = timed(lambda: split(True))
-res["split_retrieve_ms"], _ = timed(lambda: split(False))
+res["stable_split_insert_ms"], _ = timed(lambda: split(True))
+res["stable_split_retrieve_ms"], _ = timed(lambda: split(False))
+# the one-pass partition ShardedTable uses (ch_route_part32, fixed-capacity segments)
+cap = int(n / S * 1.05) + 4096
+kp, vp = torch.empty(S * cap, dtype=keys.dtype, device=dev), torch.empty(S * cap, dtype=vals.dtype, device=dev)
+cnt = torch.empty(S, dtype=torch.int64, device=dev)
+flag = torch.empty(1, dtype=torch.int32, device=dev)
+
+
+def part(with_vals):
+    _lib.check(_lib.lib().ch_route_part32(keys.data_ptr(), vals.data_ptr() if with_vals else None, n, S, cap,
+                                          perm.data_ptr(), cnt.data_ptr(), kp.data_ptr(),
+                                          vp.data_ptr() if with_vals else None, flag.data_ptr(), 0, strm()))
+
+
+res["split_insert_ms"], _ = timed(lambda: part(True))
+res["split_retrieve_ms"], _ = timed(lambda: part(False))
+assert int(flag.item()) == 0
 st = torch.zeros(n, dtype=torch.uint8, device=dev)
 out8 = torch.empty_like(st)
 res["scatter_status_ms"], _ = timed(lambda: gather_device32(st, perm, out8))
