@@ -520,8 +520,16 @@ __global__ void __launch_bounds__(PT, CH_AB_GATHER_MINB) k_st_gather(uint64_t n,
   TileGeo g;
   if (t >= ntiles || !tile_geo<L>(t, n, P, s_sup, g)) return;
   if (skip) {
-    if (L == 1)
-      for (uint32_t li = threadIdx.x; li < g.cnt; li += PT) dst_f[g.pos0 + li] = ST_INSERTED;
+    if (L == 1) {  // 16-byte stores where the tile's status range is aligned
+      uint8_t* d = dst_f + g.pos0;
+      const uint32_t head = (uint32_t)((16u - ((uintptr_t)d & 15u)) & 15u) < g.cnt ? (uint32_t)((16u - ((uintptr_t)d & 15u)) & 15u) : g.cnt;
+      for (uint32_t li = threadIdx.x; li < head; li += PT) d[li] = ST_INSERTED;
+      const uint32_t nv = (g.cnt - head) / 16;
+      const uint4 fill = make_uint4(0x01010101u * ST_INSERTED, 0x01010101u * ST_INSERTED, 0x01010101u * ST_INSERTED,
+                                    0x01010101u * ST_INSERTED);
+      for (uint32_t q = threadIdx.x; q < nv; q += PT) reinterpret_cast<uint4*>(d + head)[q] = fill;
+      for (uint32_t li = head + nv * 16 + threadIdx.x; li < g.cnt; li += PT) d[li] = ST_INSERTED;
+    }
     return;
   }
   // ib: inverse rank | bucket of bucketed slot it * PT + tid << 16.  Lookups (VAL) take the
@@ -1216,13 +1224,11 @@ constexpr uint32_t FP_TOMB = 0x81u;
 // region's keys, which leaves ~5-8% more keys past window 0 than the lane-refill pass did.
 constexpr uint32_t IQ_STEP = CH_IQ_STEP;
 
-__global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, const uint32_t* __restrict__ keys,
-                                                        const uint32_t* __restrict__ vals,
-                                                        const uint16_t* __restrict__ los,
-                                                        uint8_t* __restrict__ status, DeferOut DA, DeferOut DB, int g,
-                                                        unsigned long long* __restrict__ exc,
-                                                        const uint8_t* __restrict__ only, int fresh) {
-  if (only && !only[blockIdx.x]) return;  // after k_st_insert_sg: the regions it handed back
+__device__ __forceinline__ void insert_q_region(uint32_t f, const TableRef& T, const Part& P,
+                                                const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                                const uint16_t* __restrict__ los, uint8_t* __restrict__ status,
+                                                const DeferOut& DA, const DeferOut& DB, int g,
+                                                unsigned long long* __restrict__ exc, int fresh) {
   extern __shared__ __align__(128) unsigned char dsm[];
   uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
   uint32_t* fp32 = reinterpret_cast<uint32_t*>(tile + ST_R + TILE_PAD);
@@ -1235,7 +1241,6 @@ __global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, cons
   __shared__ uint32_t s_qn;
   __shared__ __align__(8) uint64_t bar;
   __shared__ int dirty;
-  const uint32_t f = blockIdx.x;
   uint64_t k0;
   uint32_t m;
   if (P.foff) {
@@ -1424,6 +1429,26 @@ __global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, cons
   long long* const dst[6] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
                              &T.ctr->occupied, (long long*)exc, (long long*)&T.ctr->deferred};
   cta_add<6>(cv6, dst);
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_addr(&bar)) : "memory");
+}
+
+// Regions k_st_insert_sg handed back (list, device-counted; a few CTAs loop over them), or
+// every region (list == nullptr: one CTA per region).
+__global__ void __launch_bounds__(LQT, 2) k_st_insert_q(TableRef T, Part P, const uint32_t* __restrict__ keys,
+                                                        const uint32_t* __restrict__ vals,
+                                                        const uint16_t* __restrict__ los,
+                                                        uint8_t* __restrict__ status, DeferOut DA, DeferOut DB, int g,
+                                                        unsigned long long* __restrict__ exc,
+                                                        const uint32_t* __restrict__ list,
+                                                        const unsigned long long* __restrict__ n_list, int fresh) {
+  if (!list) {
+    insert_q_region(blockIdx.x, T, P, keys, vals, los, status, DA, DB, g, exc, fresh);
+    return;
+  }
+  const unsigned long long nl = *n_list;
+  for (unsigned long long idx = blockIdx.x; idx < nl; idx += gridDim.x)
+    insert_q_region(list[idx], T, P, keys, vals, los, status, DA, DB, g, exc, fresh);
 }
 constexpr size_t insert_q_smem() { return (size_t)(ST_R + TILE_PAD) * 8 + FP_BYTES + IQ_CAP * 16; }
 
@@ -1543,7 +1568,8 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
                                                          const uint16_t* __restrict__ los,
                                                          uint8_t* __restrict__ status, DeferOut DA, DeferOut DB,
                                                          int g, unsigned long long* __restrict__ exc,
-                                                         uint8_t* __restrict__ redo, int fresh) {
+                                                         uint32_t* __restrict__ redo,
+                                                         unsigned long long* __restrict__ n_redo, int fresh) {
   extern __shared__ __align__(128) unsigned char dsm[];
   uint64_t* tile = reinterpret_cast<uint64_t*>(dsm);
   // per window start lo: participants (bits 0..15) | signature of their key hashes (16..31);
@@ -1573,7 +1599,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   }
   if (m == 0 && !fresh) return;  // (a pending clear still writes the region: fresh)
   if (m > SG_MAXK) {  // skewed region: the concurrent pass takes it
-    if (threadIdx.x == 0) redo[f] = 1;
+    if (threadIdx.x == 0) redo[atomicAdd(n_redo, 1ull)] = f;
     return;
   }
   const uint64_t rbase = (uint64_t)f << ST_LOG_R;
@@ -1654,7 +1680,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     }
     __syncthreads();
     if (s_tomb) {  // tombstones: the deferred-claim rule needs the concurrent pass
-      if (threadIdx.x == 0) redo[f] = 1;
+      if (threadIdx.x == 0) redo[atomicAdd(n_redo, 1ull)] = f;
       return;
     }
     const uint32_t fc = threadIdx.x < ST_R / 32 ? __popc(freew[threadIdx.x]) : 0u;
@@ -1812,7 +1838,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   }
   __syncthreads();
   if (s_dup) {
-    if (threadIdx.x == 0) redo[f] = 1;
+    if (threadIdx.x == 0) redo[atomicAdd(n_redo, 1ull)] = f;
     return;
   }
   // (f) results: statuses, deferrals, counters
@@ -1922,7 +1948,7 @@ struct Round {
   uint16_t* lo2;
   uint16_t *inv1, *inv2, *th1, *th2;  // inverse (round 1 only)
   uint8_t *bid1, *bid2;               // bucket of each bucketed slot per tile (round 1 only)
-  uint8_t* redo;                      // regions k_st_insert_sg hands to k_st_insert_q (round 1 only)
+  uint8_t* redo;                      // regions k_st_insert_sg hands to k_st_insert_q: count, list
   uint32_t *tg1, *tg2;
 };
 
@@ -1964,7 +1990,7 @@ static void carve_round(Carver& c, Round& r, const StPlan& p, uint64_t n, int np
   if (inverse) {
     r.inv1 = (uint16_t*)c.take(n * 2);
     r.inv2 = (uint16_t*)c.take(n1 * 2);
-    r.redo = (uint8_t*)c.take(p.regions);
+    r.redo = (uint8_t*)c.take(64 + p.regions * 4ull);  // count, then the handed-back region list
     r.bid1 = npay == 0 ? (uint8_t*)c.take(n) : nullptr;  // lookups only (k_st_gather<L, true>)
     r.bid2 = npay == 0 ? (uint8_t*)c.take(n1) : nullptr;
     r.th1 = (uint16_t*)c.take(p.tiles1 * p.supers * 2);
@@ -2176,23 +2202,27 @@ static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const 
     const size_t sm = insert_q_smem();
     int rc = st_smem(k_st_insert_q, sm);
     if (rc) return rc;
-    const uint8_t* only = nullptr;
+    const uint32_t* list = nullptr;
+    unsigned long long* n_list = reinterpret_cast<unsigned long long*>(r.redo);
+    uint32_t* redo = reinterpret_cast<uint32_t*>(r.redo + 64);
     if (g_insert_sg) {
       const size_t sm2 = insert_sg_smem();
       if ((rc = st_smem(k_st_insert_sg, sm2))) return rc;
-      if ((rc = cuda_check(cudaMemsetAsync(r.redo, 0, p.regions, lc.stream), "memset"))) return rc;
+      if ((rc = cuda_check(cudaMemsetAsync(n_list, 0, 8, lc.stream), "memset"))) return rc;
       st_timed(lc, &e0);
       k_st_insert_sg<<<p.regions, SGT, sm2, lc.stream>>>(T, r.part, r.k2, r.v2, r.lo2, status, DA, DB, g, exc,
-                                                         r.redo, fresh);
+                                                         redo, n_list, fresh);
       count_launch();
       st_timed_end(lc, e0);
       if ((rc = cuda_check(cudaGetLastError(), "staged sorted insert"))) return rc;
-      only = r.redo;
+      list = redo;
     } else {
       st_timed(lc, &e0);
     }
-    k_st_insert_q<<<p.regions, LQT, sm, lc.stream>>>(T, r.part, r.k2, r.v2, r.lo2, status, DA, DB, g, exc, only,
-                                                     fresh);
+    // the handed-back regions: a few CTAs loop over the list (usually empty)
+    const unsigned qgrid = list ? (unsigned)(lc.sms * 2) : p.regions;
+    k_st_insert_q<<<qgrid, LQT, sm, lc.stream>>>(T, r.part, r.k2, r.v2, r.lo2, status, DA, DB, g, exc, list, n_list,
+                                                 fresh);
     count_launch();
     if (!g_insert_sg) st_timed_end(lc, e0);
     return cuda_check(cudaGetLastError(), "staged region insert");
