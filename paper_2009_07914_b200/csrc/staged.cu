@@ -608,6 +608,130 @@ __global__ void __launch_bounds__(PT, CH_AB_GATHER_MINB) k_st_gather(uint64_t n,
   }
 }
 
+// The status gathers (inserts): the same inverse as k_st_gather, run as a few persistent
+// CTAs over the tiles; without exceptions (the common case) level 1 fills the caller's
+// statuses with INSERTED grid-stride and nothing else runs -- no 65 K-CTA launch.
+template <int L, bool VAL>
+__global__ void __launch_bounds__(PT, CH_AB_GATHER_MINB) k_st_gather_st(uint64_t n, Part P, uint32_t supers, uint32_t ntiles,
+                                                  const uint16_t* __restrict__ inv,
+                                                  const uint16_t* __restrict__ th, const uint32_t* __restrict__ tg,
+                                                  uint32_t nb, const uint32_t* __restrict__ src_v,
+                                                  const uint8_t* __restrict__ src_f, uint32_t* __restrict__ dst_v,
+                                                  uint8_t* __restrict__ dst_f,
+                                                  const unsigned long long* __restrict__ exc,
+                                                  const uint8_t* __restrict__ bid) {
+  __shared__ uint32_t sV[VAL ? PTILE : 1];
+  __shared__ uint8_t sF[PTILE];
+  __shared__ uint16_t sB[VAL ? 1 : PTILE];  // statuses: bucket of each bucketed slot
+  __shared__ uint32_t gsrc[PBINS];
+  __shared__ uint32_t wt[PT / 32];
+  __shared__ uint32_t s_sup[4];
+  // every status INSERTED (insert without exceptions): nothing to move back; level 1 fills
+  // the caller's statuses grid-stride with 16-byte stores (the status gathers run as a few
+  // persistent CTAs, so the common case costs no 65 K-CTA launch)
+  if (!VAL && exc && *exc == 0) {
+    if (L == 1) {
+      const uint32_t head = (uint32_t)((16u - ((uintptr_t)dst_f & 15u)) & 15u) < n ? (uint32_t)((16u - ((uintptr_t)dst_f & 15u)) & 15u) : (uint32_t)n;
+      const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, gstr = (uint64_t)gridDim.x * blockDim.x;
+      if (gtid < head) dst_f[gtid] = ST_INSERTED;
+      const uint64_t nv = (n - head) / 16;
+      const uint4 fill = make_uint4(0x01010101u * ST_INSERTED, 0x01010101u * ST_INSERTED, 0x01010101u * ST_INSERTED,
+                                    0x01010101u * ST_INSERTED);
+      for (uint64_t q = gtid; q < nv; q += gstr) reinterpret_cast<uint4*>(dst_f + head)[q] = fill;
+      for (uint64_t li = head + nv * 16 + gtid; li < n; li += gstr) dst_f[li] = ST_INSERTED;
+    }
+    return;
+  }
+  auto one_tile = [&](const uint32_t t) {
+  // the run table depends on t only: in flight while the geometry resolves
+  const bool rt = threadIdx.x < nb;
+  const uint32_t hv = rt ? th[(uint64_t)t * nb + threadIdx.x] : 0u;
+  const uint32_t gs = rt ? tg[(uint64_t)t * nb + threadIdx.x] : 0u;
+  if (L == 2) tile_super(t, P, supers, s_sup);
+  TileGeo g;
+  if (t >= ntiles || !tile_geo<L>(t, n, P, s_sup, g)) return;
+  // ib: inverse rank | bucket of bucketed slot it * PT + tid << 16.  Lookups (VAL) take the
+  // buckets from the split (bid, 1 B per key: 1.03 -> 0.94 ms per level at 2^28); inserts,
+  // whose gathers run only after exceptions, rebuild them from the run table (thread b
+  // writes its run's slots).  Full, aligned lookup tiles (vec) write the caller's order four
+  // keys per thread: 16-byte value and 4-byte flag stores, 8-byte inverse-rank loads.
+  const bool vec = VAL && L == 1 && g.cnt == PTILE && ((g.pos0 & 3) == 0) && (((uintptr_t)(dst_v + g.pos0) & 15) == 0) &&
+                   (((uintptr_t)(dst_f + g.pos0) & 3) == 0);
+  uint32_t ib[PI];
+  uint2 iv4[PI / 4];
+  if (vec) {
+#pragma unroll
+    for (int h = 0; h < PI / 4; ++h)
+      iv4[h] = __ldcs(reinterpret_cast<const uint2*>(inv + g.pos0) + h * PT + threadIdx.x);
+#pragma unroll
+    for (int it = 0; it < PI; ++it) ib[it] = (uint32_t)__ldcs(bid + g.pos0 + (uint32_t)it * PT + threadIdx.x) << 16;
+  } else {
+#pragma unroll
+    for (int it = 0; it < PI; ++it) {  // inverse ranks (and bucket ids) load alongside the run table
+      const uint32_t li = (uint32_t)it * PT + threadIdx.x;
+      ib[it] = li < g.cnt ? (uint32_t)__ldcs(inv + g.pos0 + li) |
+                                (VAL ? (uint32_t)__ldcs(bid + g.pos0 + li) << 16 : 0u)
+                          : 0u;
+    }
+  }
+  const uint32_t bo = block_excl_scan(hv, wt);
+  gsrc[threadIdx.x] = gs - bo;  // run source minus its tile offset
+  if (!VAL) {
+    __syncthreads();
+    for (uint32_t x = 0; x < hv; ++x) sB[bo + x] = (uint16_t)threadIdx.x;
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < PI; ++it) ib[it] |= (uint32_t)sB[(uint32_t)it * PT + threadIdx.x] << 16;
+  }
+  __syncthreads();
+  uint32_t v[PI];
+  uint8_t fl[PI];
+#pragma unroll
+  for (int it = 0; it < PI; ++it) {
+    const uint32_t j = (uint32_t)it * PT + threadIdx.x;
+    if (j < g.cnt) {
+      const uint32_t src = gsrc[ib[it] >> 16] + j;
+      if (VAL) v[it] = src_v[src];
+      fl[it] = src_f[src];
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < PI; ++it) {
+    const uint32_t j = (uint32_t)it * PT + threadIdx.x;
+    if (j < g.cnt) {
+      if (VAL) sV[j] = v[it];
+      sF[j] = fl[it];
+    }
+  }
+  __syncthreads();
+  if (vec) {
+#pragma unroll
+    for (int h = 0; h < PI / 4; ++h) {
+      const uint32_t li = 4u * ((uint32_t)h * PT + threadIdx.x);
+      const uint32_t j0 = iv4[h].x & 0xFFFFu, j1 = iv4[h].x >> 16, j2 = iv4[h].y & 0xFFFFu, j3 = iv4[h].y >> 16;
+      *reinterpret_cast<uint4*>(dst_v + g.pos0 + li) = make_uint4(sV[j0], sV[j1], sV[j2], sV[j3]);
+      *reinterpret_cast<uint32_t*>(dst_f + g.pos0 + li) =
+          (uint32_t)sF[j0] | (uint32_t)sF[j1] << 8 | (uint32_t)sF[j2] << 16 | (uint32_t)sF[j3] << 24;
+    }
+    return;
+  }
+#pragma unroll
+  for (int it = 0; it < PI; ++it) {
+    const uint32_t li = (uint32_t)it * PT + threadIdx.x;
+    if (li < g.cnt) {
+      const uint32_t j = ib[it] & 0xFFFFu;
+      if (VAL) dst_v[g.pos0 + li] = sV[j];
+      dst_f[g.pos0 + li] = sF[j];
+    }
+  }
+  };
+  // lookups: one CTA per tile; statuses: persistent CTAs over the tiles
+  for (uint32_t t = blockIdx.x; t < ntiles; t += VAL ? ntiles : gridDim.x) {
+    one_tile(t);
+    if (!VAL) __syncthreads();  // shared buffers are reused by the next tile
+  }
+}
+
 // ------------------------------------------------------------- region pass
 // Keys that window 0 cannot decide are buffered in shared memory and appended to
 // the device-counted list in batches (one global atomic per flush: a per-warp
@@ -2180,12 +2304,14 @@ static int st_backward(const Launch& lc, const StPlan& p, const StBufs& b, uint6
                        const uint8_t* rf, uint32_t* out_v, uint8_t* out_f, const unsigned long long* exc = nullptr) {
   const Round& r = b.r1;
   const unsigned t1 = (unsigned)p.tiles1, t2 = (unsigned)p.tiles2;
-  auto g2 = k_st_gather<2, VAL>;
-  auto g1 = k_st_gather<1, VAL>;
-  g2<<<t2, PT, 0, lc.stream>>>(n, r.part, p.supers, t2, r.inv2, r.th2, r.tg2, 256, rv, rf, b.rv1, b.rf1, exc,
+  auto g2 = VAL ? k_st_gather<2, VAL> : k_st_gather_st<2, VAL>;
+  auto g1 = VAL ? k_st_gather<1, VAL> : k_st_gather_st<1, VAL>;
+  const unsigned q2 = VAL ? t2 : std::min<unsigned>(t2, (unsigned)lc.sms * 3);
+  const unsigned q1 = VAL ? t1 : std::min<unsigned>(t1, (unsigned)lc.sms * 3);
+  g2<<<q2, PT, 0, lc.stream>>>(n, r.part, p.supers, t2, r.inv2, r.th2, r.tg2, 256, rv, rf, b.rv1, b.rf1, exc,
                                r.bid2);
   count_launch();
-  g1<<<t1, PT, 0, lc.stream>>>(n, r.part, p.supers, t1, r.inv1, r.th1, r.tg1, p.supers, b.rv1, b.rf1, out_v, out_f,
+  g1<<<q1, PT, 0, lc.stream>>>(n, r.part, p.supers, t1, r.inv1, r.th1, r.tg1, p.supers, b.rv1, b.rf1, out_v, out_f,
                                 exc, r.bid1);
   count_launch();
   return cuda_check(cudaGetLastError(), "staged gather");
