@@ -31,14 +31,14 @@ data = [(int(x[ia], 16), int(x[ii] or 0), int(x[isamp] or 0), int(x[ith] or 0)) 
 base = min(d[0] for d in data)
 # nvdisasm line table for the kernel
 m = re.search(r"chb::(\w+)(?:<([^>]*)>)?\(", kname)
-frag = "".join(f"L{'b' if ty == 'bool' else 'i'}{val}E" for ty, val in re.findall(r"\((\w+)\)(\d+)", m.group(2) or ""))
+frag = "".join(f"L{'b' if ty == 'bool' else 'i'}{val}E" for ty, val in re.findall(r"\((\w+)\)(\d+)(?=[,>]|$)", m.group(2) or ""))
 dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout.split("\n")
 sec, line, lines = None, None, {}
 for ln in dis:
     if ln.startswith("//--------------------- .text."):
         sec = ln.split(".text.")[1].split(" ")[0]
         continue
-    if sec is None or m.group(1) not in sec or (frag and f"I{frag}E" not in sec):
+    if sec is None or m.group(1) not in sec or (frag and f"{frag}E" not in sec):
         continue
     mm = re.match(r"\s*//## File \"([^\"]+)\", line (\d+)", ln)
     if mm:
