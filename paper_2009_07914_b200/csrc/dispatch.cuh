@@ -169,6 +169,11 @@ int table_reduce(const Launch& lc, const TableRef& T, const TypeSel& ts, unsigne
 int exclusive_scan_u32(const Launch& lc, const uint32_t* counts, uint64_t n, uint64_t* out, void* scratch,
                        size_t scratch_bytes);
 size_t exclusive_scan_scratch_bytes(uint64_t n);
+// stable LSD radix sort of (key, payload) pairs by the whole key (rsort.cu)
+size_t radix_sort_scratch_bytes(uint64_t n, int kbytes, int pbytes);
+template <typename K, typename P>
+int radix_sort_pairs(const Launch& lc, const K* kin, const P* pin, K* kout, P* pout, uint64_t n, void* scratch,
+                     size_t scratch_bytes);
 int exclusive_scan_u64(const Launch& lc, const uint64_t* counts, uint64_t n, uint64_t* out, void* scratch,
                        size_t scratch_bytes);
 

@@ -6,9 +6,9 @@
 // winner per slot).  With Zipf-distributed keys (BASELINE configs[2]: 2^27 pairs over
 // 2^23 ranks, the hottest key ~23K copies) that serialises the batch (1.7 G pairs/s).
 //
-// Here the batch is grouped by key first -- a radix sort of (key, position) pairs
-// (CUB's DeviceRadixSort as a sort primitive; a hash-table grouping pass was tried
-// first and cost 26 ms of random DRAM traffic) -- and then ONE warp per distinct key
+// Here the batch is grouped by key first -- a stable radix sort of (key, position) pairs
+// (rsort.cu; CUB's DeviceRadixSort with CH_MG_CUB=1; a hash-table grouping pass was
+// tried first and cost 26 ms of random DRAM traffic) -- and then ONE warp per distinct key
 // walks the key's sequence once: it loads a 32-slot window (a slot per lane), claims
 // the free cells it needs with CAS in lane (= sequence) order, and writes the group's
 // values into the cells it won.  The result is the state the reference reaches by
@@ -17,6 +17,7 @@
 // counters are computed from the sequence positions, exactly as the reference counts
 // them (single_table.py:197).
 #include <cub/device/device_radix_sort.cuh>
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -496,12 +497,18 @@ static int g_mw = [] {
   return v >= 1 && v <= 4 ? v : 4;
 }();
 
+// CH_MG_CUB=1: CUB's DeviceRadixSort for the grouping sort instead of rsort.cu's
+static bool g_mg_cub = [] {
+  const char* e = getenv("CH_MG_CUB");
+  return e && e[0] == '1';
+}();
+
 template <typename K, typename P>
 static size_t sort_temp_bytes(uint64_t n) {
   size_t tb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, (const K*)nullptr, (K*)nullptr, (const P*)nullptr, (P*)nullptr,
                                   (int)n);
-  return tb;
+  return std::max(tb, radix_sort_scratch_bytes(n, (int)sizeof(K), (int)sizeof(P)));
 }
 
 size_t mgroup_scratch_bytes(uint64_t n, int kbytes, int vbytes) {
@@ -548,10 +555,14 @@ static int mgroup_impl(const Launch& lc, const TableRef& T, int g, const K* keys
   const unsigned grid = (unsigned)(lc.sms * 8);
   k_mg_payload<P, V><<<grid, MG_THREADS, 0, lc.stream>>>(idx, vals, n);
   count_launch();
-  rc = cuda_check(cub::DeviceRadixSort::SortPairs(sort_tmp, sort_b, keys, sk, idx, sidx, (int)n, 0,
-                                                  (int)(8 * sizeof(K)), lc.stream),
-                  "sort by key");
-  count_launch(sizeof(K) == 8 ? 8 : 4);  // onesweep passes (approximate launch count)
+  if (g_mg_cub) {
+    rc = cuda_check(cub::DeviceRadixSort::SortPairs(sort_tmp, sort_b, keys, sk, idx, sidx, (int)n, 0,
+                                                    (int)(8 * sizeof(K)), lc.stream),
+                    "sort by key");
+    count_launch(sizeof(K) == 8 ? 8 : 4);  // onesweep passes (approximate launch count)
+  } else {
+    rc = radix_sort_pairs<K, P>(lc, keys, idx, sk, sidx, n, sort_tmp, sort_b);  // stable, by key
+  }
   if (rc) return rc;
   k_mg_heads<K><<<grid, MG_THREADS, 0, lc.stream>>>(sk, n, head);
   count_launch();

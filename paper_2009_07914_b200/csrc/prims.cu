@@ -54,28 +54,47 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_tile_sums(const TIn* __restric
   if (threadIdx.x == 0) sums[blockIdx.x] = tot;
 }
 
-// out[i] = prefix[tile] + exclusive sum within the tile; out[n] = grand total
+// out[i] = prefix[tile] + exclusive sum within the tile; out[n] = grand total.  The tile
+// goes through shared memory both ways (coalesced loads and stores; each thread scans 16
+// consecutive elements there -- a blocked layout straight from global memory put every
+// lane of a warp on its own line and measured 0.89 ms for 2^27 counts)
+__device__ __forceinline__ uint32_t scan_pad(uint32_t j) { return j + (j >> 4); }
 template <typename TIn>
 __global__ void __launch_bounds__(SCAN_THREADS) k_tile_scan(const TIn* __restrict__ in, uint64_t n,
                                                            const uint64_t* __restrict__ prefix,
                                                            uint64_t* __restrict__ out) {
-  const uint64_t base = blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_ITEMS;
+  __shared__ uint64_t st[SCAN_TILE + SCAN_TILE / 16];
+  const uint64_t tb = (uint64_t)blockIdx.x * SCAN_TILE;
+  const uint64_t pre = prefix ? prefix[blockIdx.x] : 0;
+#pragma unroll
+  for (int r = 0; r < SCAN_ITEMS; ++r) {
+    const uint32_t j = (uint32_t)r * SCAN_THREADS + threadIdx.x;
+    const uint64_t i = tb + j;
+    st[scan_pad(j)] = i < n ? (uint64_t)in[i] : 0;
+  }
+  __syncthreads();
   uint64_t v[SCAN_ITEMS];
   uint64_t s = 0;
 #pragma unroll
   for (int r = 0; r < SCAN_ITEMS; ++r) {
-    const uint64_t i = base + r;
-    v[r] = i < n ? (uint64_t)in[i] : 0;
+    v[r] = st[scan_pad(threadIdx.x * SCAN_ITEMS + r)];
     s += v[r];
   }
   uint64_t tot;
-  uint64_t run = block_exclusive_sum<uint64_t>(s, &tot) + (prefix ? prefix[blockIdx.x] : 0);
+  uint64_t run = block_exclusive_sum<uint64_t>(s, &tot) + pre;  // syncs
 #pragma unroll
   for (int r = 0; r < SCAN_ITEMS; ++r) {
-    const uint64_t i = base + r;
-    if (i < n) out[i] = run;
+    const uint32_t j = threadIdx.x * SCAN_ITEMS + r;
+    st[scan_pad(j)] = run;
     run += v[r];
-    if (i == n - 1) out[n] = run;
+    if (tb + j == n - 1) out[n] = run;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < SCAN_ITEMS; ++r) {
+    const uint32_t j = (uint32_t)r * SCAN_THREADS + threadIdx.x;
+    const uint64_t i = tb + j;
+    if (i < n) out[i] = st[scan_pad(j)];
   }
 }
 

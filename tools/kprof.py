@@ -1,0 +1,46 @@
+"""Per-kernel device times of the multi-value grouped insert, without a replaying profiler.
+
+  python tools/kprof.py [log2 n]      (CUPTI activity records through torch.profiler)
+"""
+import math
+import os
+import sys
+from collections import defaultdict
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from torch.profiler import ProfilerActivity, profile
+
+from paper_2009_07914_b200 import MultiValueHashTable
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from bench_configs import zipf_keys  # noqa: E402
+
+n = 1 << (int(sys.argv[1]) if len(sys.argv) > 1 else 27)
+dev = torch.device("cuda", 0)
+keys, _ = zipf_keys(n, 1 << 23, 0.5, 42, dev)
+k32 = keys.to(torch.int32)
+v32 = torch.arange(1, n + 1, device=dev, dtype=torch.int32)
+for rep in range(3):
+    t = MultiValueHashTable(math.ceil(n / 0.8), layout="packed", key_bits=32, value_bits=32, group_width=8,
+                            device=0)
+    torch.cuda.synchronize()
+    if rep < 2:
+        t.insert_device(k32, v32)
+        torch.cuda.synchronize()
+        continue
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        t.insert_device(k32, v32)
+        torch.cuda.synchronize()
+tot = defaultdict(float)
+cnt = defaultdict(int)
+for e in prof.events():
+    if e.device_type == torch.autograd.DeviceType.CUDA:
+        name = e.name[:60]
+        tot[name] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+        cnt[name] += 1
+s = 0.0
+for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+    print(f"{v / 1000:8.3f} ms  x{cnt[k]:2d}  {k}")
+    s += v
+print(f"{s / 1000:8.3f} ms  total")
