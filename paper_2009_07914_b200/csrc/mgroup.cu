@@ -41,21 +41,95 @@ __global__ void k_mg_payload(P* __restrict__ x, const V* __restrict__ vals, uint
 template <typename P>
 __device__ __forceinline__ uint32_t pay_idx(P p) { return sizeof(P) == 8 ? (uint32_t)(p >> 32) : (uint32_t)p; }
 
-// head[i] = 1 where a run of equal keys starts in the sorted batch
+// Runs of equal keys in the sorted batch, in one pass: gstart[g] = first sorted position of
+// group g, gstart[ngroups] = n, *ngroups.  Tiles of 4096 keys in start order (atomic tile
+// counter); a warp owns 256 consecutive keys (eight ballots of run heads), a block scan
+// over the warps numbers the tile's heads and a decoupled look-back by warp 0 (one status
+// word per tile: flag << 62 | heads, 32 predecessors per step) numbers the tile's first head.  (Was: head flags, a scan of
+// 2^27 u32 into u64 and a scatter -- 1.2 ms of the 2^27 Zipf insert.)
+constexpr int MR_T = 512, MR_I = 8;
+constexpr uint32_t MR_TILE = MR_T * MR_I;
+constexpr uint64_t MR_AGG = 1ull << 62, MR_INC = 2ull << 62, MR_VAL = (1ull << 62) - 1;
 template <typename K>
-__global__ void k_mg_heads(const K* __restrict__ sk, uint64_t n, uint32_t* __restrict__ head) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    head[i] = (i == 0 || sk[i] != sk[i - 1]) ? 1u : 0u;
-}
-
-// gstart[g] = first sorted position of group g; gstart[ngroups] = n
-__global__ void k_mg_starts(const uint32_t* __restrict__ head, const uint64_t* __restrict__ hoff, uint64_t n,
-                            uint32_t* __restrict__ gstart) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    if (head[i]) gstart[hoff[i]] = (uint32_t)i;
-  if (blockIdx.x == 0 && threadIdx.x == 0) gstart[hoff[n]] = (uint32_t)n;
+__global__ void __launch_bounds__(MR_T) k_mg_runs(const K* __restrict__ sk, uint64_t n, uint32_t* __restrict__ gstart,
+                                                  unsigned long long* __restrict__ ngroups,
+                                                  unsigned long long* __restrict__ status,
+                                                  unsigned int* __restrict__ next_tile) {
+  __shared__ uint32_t s_t, wsum[MR_T / 32];
+  __shared__ unsigned long long s_pre;
+  if (threadIdx.x == 0) s_t = atomicAdd(next_tile, 1u);
+  __syncthreads();
+  const uint32_t t = s_t;
+  const uint64_t base = (uint64_t)t * MR_TILE;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  K k[MR_I];
+  K before = 0;  // the key just before the warp's first (lane 0)
+#pragma unroll
+  for (int r = 0; r < MR_I; ++r) {
+    const uint64_t i = base + warp * 32u * MR_I + (uint32_t)r * 32u + lane;
+    k[r] = i < n ? sk[i] : (K)0;
+  }
+  {
+    const uint64_t i0 = base + warp * 32u * MR_I;
+    if (lane == 0 && i0 > 0 && i0 < n) before = sk[i0 - 1];
+  }
+  uint32_t bal[MR_I], cnt = 0;
+#pragma unroll
+  for (int r = 0; r < MR_I; ++r) {
+    const uint64_t i = base + warp * 32u * MR_I + (uint32_t)r * 32u + lane;
+    K prev = __shfl_up_sync(0xffffffffu, k[r], 1);
+    const K last = __shfl_sync(0xffffffffu, k[r], 31);  // the next round's lane 0 compares with it
+    if (lane == 0) prev = before;
+    before = last;
+    const bool head = i < n && (i == 0 || k[r] != prev);
+    bal[r] = __ballot_sync(0xffffffffu, head);
+    cnt += (uint32_t)__popc(bal[r]);
+  }
+  if (lane == 0) wsum[warp] = cnt;
+  __syncthreads();
+  uint32_t woff = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < MR_T / 32; ++w) {
+    const uint32_t x = wsum[w];
+    woff += w < (int)warp ? x : 0u;
+    tot += x;
+  }
+  if (warp == 0) {  // publish, then look back with the whole warp (32 predecessors per step)
+    volatile unsigned long long* const st = status;
+    if (lane == 0) st[t] = (t == 0 ? MR_INC : MR_AGG) | tot;
+    uint64_t pre = 0;
+    for (int64_t j = (int64_t)t - 1; j >= 0;) {
+      const int64_t q = j - (int64_t)lane;
+      const uint64_t sv = q >= 0 ? st[q] : MR_INC;  // before tile 0: an inclusive zero
+      const unsigned inc = __ballot_sync(0xffffffffu, (sv & MR_INC) != 0);
+      const unsigned nr = __ballot_sync(0xffffffffu, (sv & ~MR_VAL) == 0);
+      const unsigned upto = inc ? (inc & (0u - inc)) * 2u - 1u : 0xffffffffu;  // lanes through the nearest INC
+      if (nr & upto) continue;  // an unpublished tile on the way: read again
+      uint64_t v = (lane < 32u && ((upto >> lane) & 1u)) ? (sv & MR_VAL) : 0ull;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+      pre += v;
+      if (inc) break;
+      j -= 32;
+    }
+    if (lane == 0) {
+      if (t) st[t] = MR_INC | (pre + tot);
+      s_pre = pre;
+      if (base + MR_TILE >= n) {  // the last tile: the sentinel start and the group count
+        gstart[pre + tot] = (uint32_t)n;
+        *ngroups = pre + tot;
+      }
+    }
+  }
+  __syncthreads();
+  uint64_t g = s_pre + woff;
+#pragma unroll
+  for (int r = 0; r < MR_I; ++r) {
+    const uint64_t i = base + warp * 32u * MR_I + (uint32_t)r * 32u + lane;
+    if ((bal[r] >> lane) & 1u) gstart[g + (uint32_t)__popc(bal[r] & lt)] = (uint32_t)i;
+    g += (uint32_t)__popc(bal[r]);
+  }
 }
 
 // key of slot q (through L2: other SMs claim cells concurrently)
@@ -514,8 +588,8 @@ static size_t sort_temp_bytes(uint64_t n) {
 size_t mgroup_scratch_bytes(uint64_t n, int kbytes, int vbytes) {
   const size_t sort_b = kbytes == 8 ? sort_temp_bytes<uint64_t, uint64_t>(n) : sort_temp_bytes<uint32_t, uint64_t>(n);
   (void)vbytes;
-  return al256(sort_b) + al256(n * kbytes) + 2 * al256(n * 8) + al256(n * 4) + al256((n + 1) * 8) +
-         al256(exclusive_scan_scratch_bytes(n)) + 2 * al256((n + 1) * 4) + 256 + al256((n / MG_HUGE + 1) * 4);
+  return al256(sort_b) + al256(n * kbytes) + 2 * al256(n * 8) + al256((n + MR_TILE - 1) / MR_TILE * 8 + 64) +
+         al256(8) + 2 * al256((n + 1) * 4) + 256 + al256((n / MG_HUGE + 1) * 4);
 }
 
 template <Layout LAY, typename K, typename V>
@@ -537,10 +611,10 @@ static int mgroup_impl(const Launch& lc, const TableRef& T, int g, const K* keys
   K* sk = (K*)take(n * sizeof(K));
   P* idx = (P*)take(n * 8);
   P* sidx = (P*)take(n * 8);
-  uint32_t* head = (uint32_t*)take(n * 4);
-  uint64_t* hoff = (uint64_t*)take((n + 1) * 8);
-  const size_t scan_b = exclusive_scan_scratch_bytes(n);
-  void* scan = take(scan_b);
+  const uint64_t rtiles = (n + MR_TILE - 1) / MR_TILE;
+  unsigned long long* rstat = (unsigned long long*)take(rtiles * 8 + 64);  // run look-back, tile counter
+  unsigned int* rnext = (unsigned int*)(rstat + rtiles);
+  uint64_t* ngroups = (uint64_t*)take(8);
   uint32_t* gstart = (uint32_t*)take((n + 1) * 4);
   uint32_t* big = (uint32_t*)take((n + 1) * 4);
   unsigned long long* next = (unsigned long long*)take(64);  // [0] big grab, [1] big groups, [2] grab, [3] huge, [4] huge grab
@@ -564,12 +638,10 @@ static int mgroup_impl(const Launch& lc, const TableRef& T, int g, const K* keys
     rc = radix_sort_pairs<K, P>(lc, keys, idx, sk, sidx, n, sort_tmp, sort_b);  // stable, by key
   }
   if (rc) return rc;
-  k_mg_heads<K><<<grid, MG_THREADS, 0, lc.stream>>>(sk, n, head);
+  if ((rc = cuda_check(cudaMemsetAsync(rstat, 0, rtiles * 8 + 64, lc.stream), "memset"))) return rc;
+  k_mg_runs<K><<<(unsigned)rtiles, MR_T, 0, lc.stream>>>(sk, n, gstart, (unsigned long long*)ngroups, rstat, rnext);
   count_launch();
-  if ((rc = exclusive_scan_u32(lc, head, n, hoff, scan, scan_b))) return rc;
-  k_mg_starts<<<grid, MG_THREADS, 0, lc.stream>>>(head, hoff, n, gstart);
-  count_launch();
-  k_mg_big<<<grid, MG_THREADS, 0, lc.stream>>>(gstart, hoff + n, big, next + 1, huge, next + 3);
+  k_mg_big<<<grid, MG_THREADS, 0, lc.stream>>>(gstart, ngroups, big, next + 1, huge, next + 3);
   count_launch();
   if ((rc = cuda_check(cudaGetLastError(), "group runs"))) return rc;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -578,10 +650,10 @@ static int mgroup_impl(const Launch& lc, const TableRef& T, int g, const K* keys
   k_mg_place_cta<LAY, K, V, P><<<(unsigned)lc.sms, 512, 0, lc.stream>>>(T, sk, sidx, gstart, huge, next + 3, next + 4,
                                                                         vals, status, g);
   count_launch();
-  k_mg_place<LAY, K, V, P><<<grid, MG_THREADS, 0, lc.stream>>>(T, sk, sidx, gstart, hoff + n, big, next + 1, next,
+  k_mg_place<LAY, K, V, P><<<grid, MG_THREADS, 0, lc.stream>>>(T, sk, sidx, gstart, ngroups, big, next + 1, next,
                                                                 vals, status, g, g_mw);
   count_launch();
-  k_mg_small<LAY, K, V, P><<<grid, MG_THREADS, 0, lc.stream>>>(T, sk, sidx, gstart, hoff + n, vals, status, g);
+  k_mg_small<LAY, K, V, P><<<grid, MG_THREADS, 0, lc.stream>>>(T, sk, sidx, gstart, ngroups, vals, status, g);
   count_launch();
   if (e1) {
     cudaEventRecord(e1, lc.stream);
