@@ -76,6 +76,15 @@ size_t kmer_scratch_bytes(uint64_t n_windows, uint32_t sketch, uint64_t total_le
 
 using namespace chb;
 
+namespace {
+constexpr uint32_t kStashS = 64;  // values stashed per query by the multi-value count pass
+// CH_MULTI_STASH=0: the retrieve pass always walks again
+const bool g_multi_stash = [] {
+  const char* e = getenv("CH_MULTI_STASH");
+  return !(e && e[0] == '0');
+}();
+}  // namespace
+
 struct ch_table {
   ch_config cfg;
   TypeSel ts;          // storage types of the slot array
@@ -106,6 +115,14 @@ struct ch_table {
   // staged insert starts every region empty and writes every region (staged.cu, fresh); any other
   // operation performs the clear first (Ordered, ch_read_slot_range).  CH_LAZY_CLEAR=0: always eager.
   bool pending_clear = false;
+  // multi-value count -> retrieve: the count pass stashes the first kStashS values of every short
+  // chain (multi.cu, MultiStashMeta); the next call, if it is ch_multi_retrieve of the same keys
+  // buffer and count, copies them instead of walking again.  Any other call invalidates it.
+  void* stash = nullptr;
+  size_t stash_cap = 0;
+  bool stash_valid = false;
+  const void* stash_keys = nullptr;
+  uint64_t stash_n = 0;
 };
 
 namespace {
@@ -144,6 +161,7 @@ struct Ordered {
     lc.device = t->cfg.device;
     lc.sms = t->sms;
     lc.timer = t->timing ? &t->timer : nullptr;
+    t->stash_valid = false;  // consumed or invalidated by every operation (ch_multi_retrieve)
     cudaStreamWaitEvent(s, t->last, 0);
     if (t->pending_clear && !lazy_ok) {
       Launch c = lc;
@@ -423,6 +441,7 @@ int ch_destroy(ch_table* t) {
   cudaFree(t->winfo);
   cudaFree(t->gsizes);
   cudaFree(t->gsums);
+  cudaFree(t->stash);
   if (t->last) cudaEventDestroy(t->last);
   delete t;
   return CH_OK;
@@ -658,13 +677,36 @@ int ch_multi_count(ch_table* t, const void* keys, uint64_t n, uint32_t* counts, 
   uint32_t* ll = (uint32_t*)sc.get(n * 4 + 16);
   unsigned long long* lc2 = (unsigned long long*)sc.get(multi_scan_counter_bytes());
   if (!ll || !lc2) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
-  int rc = multi_scan(o.lc, t->T, t->ts, keys, n, counts, nullptr, nullptr, 0, ll, lc2);
+  // the stash for the retrieve pass that usually follows (batches of >= 4096 queries, <= 4 GiB)
+  void* stash = nullptr;
+  void* meta = nullptr;
+  const size_t sv = (size_t)n * kStashS * (size_t)t->vbytes, need = sv + (size_t)n * sizeof(MultiStashMeta) + 256;
+  if (g_multi_stash && n >= 4096 && need <= (4ull << 30)) {
+    if (t->stash_cap < need) {  // stream-ordered: the pool keeps the memory between calls
+      if (t->stash) cudaFreeAsync(t->stash, o.s);
+      t->stash = nullptr;
+      t->stash_cap = 0;
+      if (cudaMallocAsync(&t->stash, need, o.s) == cudaSuccess) t->stash_cap = need;
+      else cudaGetLastError();  // no stash: the retrieve walks again
+    }
+    if (t->stash) {
+      stash = t->stash;
+      meta = (char*)t->stash + ((sv + 255) & ~(size_t)255);
+    }
+  }
+  int rc = multi_scan(o.lc, t->T, t->ts, keys, n, counts, nullptr, nullptr, 0, ll, lc2, nullptr, stash, meta,
+                      stash ? kStashS : 0u);
   if (!rc) {
     const size_t sb = exclusive_scan_scratch_bytes(n);
     void* p = sc.get(sb);
     rc = p ? exclusive_scan_u32(o.lc, counts, n, offsets, p, sb) : fail(CH_ENOMEM, "scratch allocation failed");
   }
   t->host_ops += n;
+  if (!rc && stash) {
+    t->stash_valid = true;
+    t->stash_keys = keys;
+    t->stash_n = n;
+  }
   return o.done(rc);
 }
 
@@ -673,13 +715,27 @@ int ch_multi_retrieve(ch_table* t, const void* keys, uint64_t n, const uint64_t*
   if (!t) return fail(CH_EINVAL, "null table");
   if (t->cfg.kind != CH_MULTI) return fail(CH_EINVAL, "ch_multi_retrieve needs a multi-value table");
   if (n && (!keys || !offsets)) return fail(CH_EINVAL, "null buffer");
+  // the stash of the count pass just before, over the same keys buffer (the copy kernel also
+  // checks every query's key and count against it)
+  std::unique_lock<std::mutex> peek(t->mu);
+  const bool use = t->stash_valid && t->stash && t->stash_keys == keys && t->stash_n == n && vals_out;
+  peek.unlock();
   Ordered o(t, stream);
   t->host_ops += n;
   Scratch sc(o.s);
   uint32_t* ll = (uint32_t*)sc.get(n * 4 + 16);
   unsigned long long* lc2 = (unsigned long long*)sc.get(multi_scan_counter_bytes());
   if (!ll || !lc2) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
-  return o.done(multi_scan(o.lc, t->T, t->ts, keys, n, nullptr, offsets, vals_out, 1, ll, lc2));
+  const size_t sv = (size_t)n * kStashS * (size_t)t->vbytes;
+  const int rc = multi_scan(o.lc, t->T, t->ts, keys, n, nullptr, offsets, vals_out, 1, ll, lc2, nullptr,
+                            use ? t->stash : nullptr, use ? (char*)t->stash + ((sv + 255) & ~(size_t)255) : nullptr,
+                            use ? kStashS : 0u);
+  if (t->stash) {  // back to the pool once read (the next count pass takes it again)
+    cudaFreeAsync(t->stash, o.s);
+    t->stash = nullptr;
+    t->stash_cap = 0;
+  }
+  return o.done(rc);
 }
 
 int ch_multi_retrieve_slots(ch_table* t, const void* keys, uint64_t n, const uint64_t* offsets, void* vals_out,

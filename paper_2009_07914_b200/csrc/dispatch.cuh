@@ -159,9 +159,17 @@ int multi_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const v
 // multi_scan holds 4 words and this many 24-byte entries
 constexpr uint64_t kMultiHugeCap = 1ull << 16;
 constexpr size_t multi_scan_counter_bytes() { return 32 + kMultiHugeCap * 24; }
+// stash (count pass, mode 0): the first stash_s values of every query resolved by the thread
+// pass, and per query {key, count, attempts, windows}; the retrieve pass (mode 1) copies them
+// for queries whose key and count still match instead of walking again (MultiStashMeta)
+struct MultiStashMeta {
+  unsigned long long key;
+  uint32_t total, att, win, pad;
+};
 int multi_scan(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
                uint32_t* counts, const uint64_t* offsets, void* vals_out, int mode, uint32_t* long_list,
-               unsigned long long* counters, int64_t* slot_out = nullptr);
+               unsigned long long* counters, int64_t* slot_out = nullptr,
+               void* stash = nullptr, void* stash_meta = nullptr, uint32_t stash_s = 0);
 size_t for_all_scratch_bytes(uint64_t c);
 int table_for_all(const Launch& lc, const TableRef& T, const TypeSel& ts, void* keys_out, void* vals_out,
                   int64_t* slots_out, uint64_t cap, uint64_t* d_count, void* scratch, size_t scratch_bytes);

@@ -98,7 +98,9 @@ __global__ void __launch_bounds__(256) k_multi_scan(TableRef T, const K* __restr
                                                     const uint64_t* __restrict__ offsets,
                                                     V* __restrict__ out, int64_t* __restrict__ slot_out,
                                                     uint32_t budget, uint32_t* __restrict__ long_list,
-                                                    unsigned long long* __restrict__ long_count) {
+                                                    unsigned long long* __restrict__ long_count,
+                                                    V* __restrict__ stash, MultiStashMeta* __restrict__ meta,
+                                                    uint32_t S) {
   using P = Probe<LAY, K, V, G>;
   using Ops = typename P::Ops;
   constexpr int MCHUNK = chunk_for<K, V>();
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(256) k_multi_scan(TableRef T, const K* __restr
           }
           if (!skip) break;
           if (MODE == 0 && lane == 0) s_cnt[li] = 0;
+          if (MODE == 0 && meta) meta[cs.base + li].win = 0;
         }
         if (li >= cs.cnt) break;
         ps = ss.get(li);
@@ -159,6 +162,11 @@ __global__ void __launch_bounds__(256) k_multi_scan(TableRef T, const K* __restr
           }
         }
       }
+      if (MODE == 0 && stash && km && total < S) {  // the first S values, in probe order
+        uint64_t r = total;
+        V* const sq = stash + (uint64_t)(cs.base + li) * S;
+        for (uint32_t m = km; m && r < S; m &= m - 1, ++r) sq[r] = P::value(T, st, lowest_bit(m));
+      }
       total += (uint64_t)__popc(km);
       bool done = false;
       uint64_t attempts = 0;
@@ -171,11 +179,21 @@ __global__ void __launch_bounds__(256) k_multi_scan(TableRef T, const K* __restr
       } else if (budget && cur.j >= budget) {  // a long chain: to the warp walker
         s_long[atomicAdd(&s_nlong, 1u)] = (uint32_t)(cs.base + li);
         if (MODE == 0 && lane == 0) s_cnt[li] = 0;
+        if (MODE == 0 && meta) meta[cs.base + li].win = 0;
         active = false;
         continue;
       }
       if (done) {
         if (MODE == 0 && lane == 0) s_cnt[li] = (uint32_t)total;
+        if (MODE == 0 && meta) {
+          MultiStashMeta mt;
+          mt.key = (unsigned long long)key;
+          mt.total = (uint32_t)total;
+          mt.att = (uint32_t)attempts;
+          mt.win = total <= S ? (uint32_t)cur.windows_seen : 0u;  // 0: not stashed
+          mt.pad = 0;
+          meta[cs.base + li] = mt;
+        }
         att += (long long)attempts;
         win += (long long)cur.windows_seen;
         active = false;
@@ -478,6 +496,61 @@ __global__ void __launch_bounds__(512) k_multi_walk_cta(TableRef T, const K* __r
   cta_add<2>(v, dst);
 }
 
+// Retrieve pass from the count pass's stash: a thread per query whose key and count still
+// match its stash entry copies the values (and accounts the walk the count pass recorded,
+// the same walk the reference's second pass repeats, multi_table.py:256-295); the rest go to
+// the warp walker's list.
+template <typename K, typename V>
+__global__ void __launch_bounds__(256) k_multi_stash_copy(TableRef T, const K* __restrict__ keys, uint64_t n,
+                                                          const uint64_t* __restrict__ offsets, V* __restrict__ out,
+                                                          const V* __restrict__ stash,
+                                                          const MultiStashMeta* __restrict__ meta, uint32_t S,
+                                                          uint32_t* __restrict__ long_list,
+                                                          unsigned long long* __restrict__ long_count) {
+  long long att = 0, win = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t n_up = (n + 31) & ~(uint64_t)31;  // whole warps in the loop (ballots)
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n_up; q += stride) {
+    bool walk = false, copy = false;
+    uint64_t base = 0, m = 0;
+    if (q < n) {
+      base = offsets[q];
+      m = offsets[q + 1] - base;
+      if (m) {
+        const MultiStashMeta mt = meta[q];
+        if (mt.win && mt.key == (unsigned long long)keys[q] && mt.total == m && m <= S) {
+          copy = true;
+          att += mt.att;
+          win += mt.win;
+        } else {
+          walk = true;
+        }
+      }
+    }
+    // the warp copies its 32 queries' values one query at a time (coalesced rows)
+    unsigned cm = __ballot_sync(0xffffffffu, copy);
+    while (cm) {
+      const int j = __ffs(cm) - 1;
+      cm &= cm - 1;
+      const uint64_t qj = __shfl_sync(0xffffffffu, q, j), bj = __shfl_sync(0xffffffffu, base, j);
+      const uint32_t mj = (uint32_t)__shfl_sync(0xffffffffu, m, j);
+      const V* sq = stash + qj * S;
+      for (uint32_t r = lane; r < mj; r += 32) out[bj + r] = sq[r];
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, walk);
+    if (b) {
+      unsigned long long w0 = 0;
+      if (lane == (uint32_t)(__ffs(b) - 1)) w0 = atomicAdd(long_count, (unsigned long long)__popc(b));
+      w0 = __shfl_sync(0xffffffffu, w0, __ffs(b) - 1);
+      if (walk) long_list[w0 + __popc(b & ((1u << lane) - 1u))] = (uint32_t)q;
+    }
+  }
+  const long long v[2] = {att, win};
+  long long* const dst[2] = {(long long*)&T.ctr->attempts, (long long*)&T.ctr->windows};
+  cta_add<2>(v, dst);
+}
+
 template <Layout LAY, typename K, typename V, int G>
 struct MultiKernels {
   static int insert(const Launch& lc, const TableRef& T, const void* keys, const void* vals, uint64_t n,
@@ -494,7 +567,7 @@ struct MultiKernels {
   static constexpr uint64_t kHugeCap = kMultiHugeCap;
   static int scan(const Launch& lc, const TableRef& T, const void* keys, uint64_t n, uint32_t* counts,
                   const uint64_t* offsets, void* out, int mode, uint32_t* long_list,
-                  unsigned long long* counters, int64_t* slot_out) {
+                  unsigned long long* counters, int64_t* slot_out, void* stash, void* meta, uint32_t S) {
     if (n == 0) return 0;
     int rc = cuda_check(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), lc.stream), "memset");
     if (rc) return rc;
@@ -502,13 +575,18 @@ struct MultiKernels {
       auto kern = k_multi_scan<LAY, K, V, G, 0>;
       rc = launch_chunked(lc, T, (const void*)kern, n, (chunk_for<K, V>()), [&](dim3 g, dim3 b) {
         kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out, slot_out, kBudget, long_list,
-                                     counters);
+                                     counters, (V*)stash, (MultiStashMeta*)meta, S);
       });
+    } else if (stash && meta && out && !slot_out) {  // the count pass's stash: copy, walk the rest
+      k_multi_stash_copy<K, V><<<(unsigned)(lc.sms * 8), 256, 0, lc.stream>>>(
+          T, (const K*)keys, n, offsets, (V*)out, (const V*)stash, (const MultiStashMeta*)meta, S, long_list, counters);
+      count_launch();
+      rc = cuda_check(cudaGetLastError(), "multi stash copy");
     } else {
       auto kern = k_multi_scan<LAY, K, V, G, 1>;
       rc = launch_chunked(lc, T, (const void*)kern, n, (chunk_for<K, V>()), [&](dim3 g, dim3 b) {
         kern<<<g, b, 0, lc.stream>>>(T, (const K*)keys, n, counts, offsets, (V*)out, slot_out, kBudget, long_list,
-                                     counters);
+                                     counters, nullptr, nullptr, 0u);
       });
     }
     if (rc) return rc;
@@ -543,10 +621,10 @@ int multi_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const v
 }
 int multi_scan(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
                uint32_t* counts, const uint64_t* offsets, void* vals_out, int mode, uint32_t* long_list,
-               unsigned long long* counters, int64_t* slot_out) {
+               unsigned long long* counters, int64_t* slot_out, void* stash, void* stash_meta, uint32_t stash_s) {
   return dispatch_types<MultiKernels>(ts, [&](auto tag) {
     return decltype(tag)::type::scan(lc, T, keys, n, counts, offsets, vals_out, mode, long_list, counters,
-                                     slot_out);
+                                     slot_out, stash, stash_meta, stash_s);
   });
 }
 

@@ -214,3 +214,68 @@ def test_hot_chain_cta_walker():
     assert all(int(counts[i]) == want[int(k)] for i, k in enumerate(bg[:5000]))
     cnt, _ = t.count_device(q)
     assert int(cnt.cpu().numpy()[0]) == m_hot
+
+
+def _walk_retrieve(t, k, offsets):
+    """ch_multi_retrieve over a copy of the keys (another buffer: no stash, a full second walk)."""
+    from paper_2009_07914_b200 import _io, _lib
+    kc = k.clone()
+    total = int(offsets[-1].item())
+    vals = torch.zeros(total, dtype=_io.torch_dtype(t.value_bits), device=k.device)
+    _lib.check(_lib.lib().ch_multi_retrieve(t._dt.handle, kc.data_ptr(), kc.numel(), offsets.data_ptr(),
+                                            vals.data_ptr(), t._stream(None)), "multi retrieve")
+    return vals
+
+
+def test_retrieve_from_count_stash_is_exact():
+    """The retrieve pass copies the count pass's stash for short chains: values in probe order,
+    offsets and probe counters identical to walking the sequences again."""
+    n = 1 << 16
+    rng = np.random.default_rng(7)
+    ranks = np.minimum(rng.zipf(1.3, size=n), 1 << 14).astype(np.uint64)  # multiplicities 1 .. thousands
+    keys = ranks * np.uint64(2654435761) % np.uint64(1 << 31) + np.uint64(1)
+    vals = np.arange(1, n + 1, dtype=np.uint64)
+    t = MultiValueHashTable(int(np.ceil(n / 0.8)), layout="packed", key_bits=32, value_bits=32, group_width=8)
+    assert (t.insert_device(keys, vals).cpu().numpy() == 0).all()
+    q = torch.from_numpy(np.unique(keys).astype(np.int64)).to(torch.int32).cuda()
+    q = torch.cat([q, torch.tensor([12345, 0x7FFFFFF0], dtype=torch.int32, device="cuda")])  # absent keys
+    c0 = t.probe_counters()
+    offsets, flat = t.retrieve_device(q)                      # count (stash) + retrieve (copy)
+    c1 = t.probe_counters()
+    _, offsets2 = t.count_device(q)
+    flat2 = _walk_retrieve(t, q, offsets2)                    # count + full second walk
+    c2 = t.probe_counters()
+    assert torch.equal(offsets, offsets2) and int(offsets[-1]) == n
+    assert torch.equal(flat, flat2)                           # probe order, exactly
+    assert (c1.ops - c0.ops, c1.attempts - c0.attempts, c1.windows_visited - c0.windows_visited) == \
+        (c2.ops - c1.ops, c2.attempts - c1.attempts, c2.windows_visited - c1.windows_visited)
+
+
+def test_count_stash_checks_keys_and_invalidates():
+    """A key changed in place between the passes is walked (the stash entry's key differs); any
+    other operation on the table between the passes drops the stash."""
+    from paper_2009_07914_b200 import _io, _lib
+    n = 1 << 14
+    keys = np.repeat(np.arange(1, n // 4 + 1, dtype=np.uint64), 4)
+    vals = np.arange(1, n + 1, dtype=np.uint64)
+    t = MultiValueHashTable(int(np.ceil(n / 0.8)), layout="packed", key_bits=32, value_bits=32, group_width=8)
+    t.insert_device(keys, vals)
+    q = torch.arange(1, n // 4 + 1, dtype=torch.int32, device="cuda")
+    _, offsets = t.count_device(q)
+    q[3] = 9                                                  # same count (4), other values
+    vals_out = torch.zeros(int(offsets[-1]), dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().ch_multi_retrieve(t._dt.handle, q.data_ptr(), q.numel(), offsets.data_ptr(),
+                                            vals_out.data_ptr(), t._stream(None)), "multi retrieve")
+    assert torch.equal(vals_out, _walk_retrieve(t, q, offsets))
+    seg = vals_out[offsets[3]:offsets[4]].cpu().numpy()
+    assert sorted(seg.tolist()) == list(range(33, 37))        # key 9's values, not key 4's
+    # count, then an insert, then retrieve: the stash is gone, the new copy is found
+    q2 = torch.arange(1, n // 4 + 1, dtype=torch.int32, device="cuda")
+    _, off2 = t.count_device(q2)
+    t.insert_device(np.array([1], dtype=np.uint64), np.array([999999], dtype=np.uint64))
+    _, off3 = t.count_device(q2)
+    v3 = torch.zeros(int(off3[-1]), dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().ch_multi_retrieve(t._dt.handle, q2.data_ptr(), q2.numel(), off3.data_ptr(),
+                                            v3.data_ptr(), t._stream(None)), "multi retrieve")
+    assert int(off3[-1]) == int(off2[-1]) + 1 and 999999 in v3[:5].cpu().tolist()
+    assert _io is not None

@@ -1,6 +1,6 @@
 """Per-kernel device times of the multi-value grouped insert, without a replaying profiler.
 
-  python tools/kprof.py [log2 n]      (CUPTI activity records through torch.profiler)
+  python tools/kprof.py [log2 n] [insert|retrieve]   (CUPTI activity records via torch.profiler)
 """
 import math
 import os
@@ -17,6 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from bench_configs import zipf_keys  # noqa: E402
 
 n = 1 << (int(sys.argv[1]) if len(sys.argv) > 1 else 27)
+what = sys.argv[2] if len(sys.argv) > 2 else "insert"
 dev = torch.device("cuda", 0)
 keys, _ = zipf_keys(n, 1 << 23, 0.5, 42, dev)
 k32 = keys.to(torch.int32)
@@ -25,12 +26,17 @@ for rep in range(3):
     t = MultiValueHashTable(math.ceil(n / 0.8), layout="packed", key_bits=32, value_bits=32, group_width=8,
                             device=0)
     torch.cuda.synchronize()
-    if rep < 2:
+    if what == "retrieve":
         t.insert_device(k32, v32)
+        q = torch.unique(keys).to(torch.int32)
+        torch.cuda.synchronize()
+    op = (lambda: t.retrieve_device(q)) if what == "retrieve" else (lambda: t.insert_device(k32, v32))
+    if rep < 2:
+        op()
         torch.cuda.synchronize()
         continue
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        t.insert_device(k32, v32)
+        op()
         torch.cuda.synchronize()
 tot = defaultdict(float)
 cnt = defaultdict(int)
