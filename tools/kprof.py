@@ -1,6 +1,7 @@
 """Per-kernel device times of the multi-value grouped insert, without a replaying profiler.
 
-  python tools/kprof.py [log2 n] [insert|retrieve]   (CUPTI activity records via torch.profiler)
+  python tools/kprof.py [log2 n] [insert|retrieve|bucket_insert|bucket_retrieve]
+(CUPTI activity records via torch.profiler)
 """
 import math
 import os
@@ -11,20 +12,31 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from torch.profiler import ProfilerActivity, profile
 
-from paper_2009_07914_b200 import MultiValueHashTable
+from paper_2009_07914_b200 import BucketListHashTable, GrowthPolicy, MultiValueHashTable
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-from bench_configs import zipf_keys  # noqa: E402
+from bench_configs import power_law_keys, zipf_keys  # noqa: E402
 
 n = 1 << (int(sys.argv[1]) if len(sys.argv) > 1 else 27)
 what = sys.argv[2] if len(sys.argv) > 2 else "insert"
 dev = torch.device("cuda", 0)
-keys, _ = zipf_keys(n, 1 << 23, 0.5, 42, dev)
-k32 = keys.to(torch.int32)
-v32 = torch.arange(1, n + 1, device=dev, dtype=torch.int32)
+bucket = what.startswith("bucket")
+what = what.replace("bucket_", "")
+if bucket:
+    keys, distinct = power_law_keys(n, 7, dev)
+    k32 = keys.to(torch.int32)
+    v32 = torch.arange(1, n + 1, device=dev, dtype=torch.int64)
+else:
+    keys, _ = zipf_keys(n, 1 << 23, 0.5, 42, dev)
+    k32 = keys.to(torch.int32)
+    v32 = torch.arange(1, n + 1, device=dev, dtype=torch.int32)
 for rep in range(3):
-    t = MultiValueHashTable(math.ceil(n / 0.8), layout="packed", key_bits=32, value_bits=32, group_width=8,
-                            device=0)
+    if bucket:
+        t = BucketListHashTable(math.ceil(distinct / 0.8), int(n * 2.5) + 64, growth=GrowthPolicy(1, 1.1),
+                                key_bits=32, value_bits=64, device=0)
+    else:
+        t = MultiValueHashTable(math.ceil(n / 0.8), layout="packed", key_bits=32, value_bits=32, group_width=8,
+                                device=0)
     torch.cuda.synchronize()
     if what == "retrieve":
         t.insert_device(k32, v32)
