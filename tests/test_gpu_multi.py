@@ -279,3 +279,28 @@ def test_count_stash_checks_keys_and_invalidates():
                                             v3.data_ptr(), t._stream(None)), "multi retrieve")
     assert int(off3[-1]) == int(off2[-1]) + 1 and 999999 in v3[:5].cpu().tolist()
     assert _io is not None
+
+
+@pytest.mark.parametrize("layout,kb,vb", [("packed", 32, 32), ("soa", 64, 64), ("aos", 32, 64)])
+def test_grouped_insert_keeps_batch_order_per_key(layout, kb, vb):
+    """The grouping sort (csrc/rsort.cu) is stable, so a key's copies are claimed in batch order
+    and come back from retrieve (probe order) exactly in batch order -- what the reference's
+    pair-by-pair inserts give (multi_table.py:113-152).  32- and 64-bit keys (4 / 8 sort passes)."""
+    n = 1 << 17
+    rng = np.random.default_rng(kb + vb)
+    ranks = np.arange(1, 2049, dtype=np.float64)
+    p = ranks ** -0.8
+    base = (rng.choice(2048, size=n, p=p / p.sum()) + 1).astype(np.uint64)
+    keys = base * np.uint64(0x9E3779B97F4A7C15 if kb == 64 else 2654435761) % np.uint64((1 << (kb - 1)) - 1) + 1
+    vals = rng.integers(0, 1 << (vb - 1), size=n, dtype=np.uint64)
+    t = MultiValueHashTable(int(np.ceil(n / 0.8)), layout=layout, key_bits=kb, value_bits=vb, group_width=8)
+    assert (t.insert_device(keys, vals).cpu().numpy() == 0).all()
+    q = np.unique(keys)
+    offsets, flat = t.retrieve_device(q)
+    offsets = offsets.cpu().numpy()
+    flat = flat.cpu().numpy().view(np.uint32 if vb == 32 else np.uint64).astype(np.uint64)
+    order = np.argsort(keys, kind="stable")                 # batch order within each key
+    sk = keys[order]
+    starts = np.searchsorted(sk, q)
+    assert (np.diff(offsets) == np.diff(np.append(starts, n))).all()
+    assert (flat == vals[order]).all()                      # q ascending = sk's key order
