@@ -227,18 +227,20 @@ def _walk_retrieve(t, k, offsets):
     return vals
 
 
-def test_retrieve_from_count_stash_is_exact():
+@pytest.mark.parametrize("layout,kb,vb", [("packed", 32, 32), ("soa", 64, 64)])
+def test_retrieve_from_count_stash_is_exact(layout, kb, vb):
     """The retrieve pass copies the count pass's stash for short chains: values in probe order,
     offsets and probe counters identical to walking the sequences again."""
     n = 1 << 16
     rng = np.random.default_rng(7)
     ranks = np.minimum(rng.zipf(1.3, size=n), 1 << 14).astype(np.uint64)  # multiplicities 1 .. thousands
     keys = ranks * np.uint64(2654435761) % np.uint64(1 << 31) + np.uint64(1)
-    vals = np.arange(1, n + 1, dtype=np.uint64)
-    t = MultiValueHashTable(int(np.ceil(n / 0.8)), layout="packed", key_bits=32, value_bits=32, group_width=8)
+    vals = np.arange(1, n + 1, dtype=np.uint64) * np.uint64(3 if vb == 64 else 1)
+    t = MultiValueHashTable(int(np.ceil(n / 0.8)), layout=layout, key_bits=kb, value_bits=vb, group_width=8)
     assert (t.insert_device(keys, vals).cpu().numpy() == 0).all()
-    q = torch.from_numpy(np.unique(keys).astype(np.int64)).to(torch.int32).cuda()
-    q = torch.cat([q, torch.tensor([12345, 0x7FFFFFF0], dtype=torch.int32, device="cuda")])  # absent keys
+    kt = torch.int32 if kb == 32 else torch.int64
+    q = torch.from_numpy(np.unique(keys).astype(np.int64)).to(kt).cuda()
+    q = torch.cat([q, torch.tensor([12345, 0x7FFFFFF0], dtype=kt, device="cuda")])  # absent keys
     c0 = t.probe_counters()
     offsets, flat = t.retrieve_device(q)                      # count (stash) + retrieve (copy)
     c1 = t.probe_counters()
