@@ -60,6 +60,8 @@ bool staged_supported(const TableRef& T, uint64_t n);
 size_t staged_scratch_bytes(const TableRef& T, uint64_t n, bool insert);
 int staged_insert(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, const void* vals,
                   uint64_t n, uint8_t* status, void* scratch, int fresh);
+int staged_erase(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
+                 uint8_t* erased, void* scratch);
 int staged_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
                   void* vals_out, uint8_t* found, void* scratch);
 size_t mgroup_scratch_bytes(uint64_t n, int kbytes, int vbytes);
@@ -77,6 +79,11 @@ size_t kmer_scratch_bytes(uint64_t n_windows, uint32_t sketch, uint64_t total_le
 using namespace chb;
 
 namespace {
+// CH_STAGED_ERASE=0: bulk erases of staged-size batches through the direct COPS kernel
+const bool g_staged_erase = [] {
+  const char* e = getenv("CH_STAGED_ERASE");
+  return !(e && e[0] == '0');
+}();
 constexpr uint32_t kStashS = 64;  // values stashed per query by the multi-value count pass
 // CH_MULTI_STASH=0: the retrieve pass always walks again
 const bool g_multi_stash = [] {
@@ -642,6 +649,12 @@ int ch_erase(ch_table* t, const void* keys, uint64_t n, uint8_t* erased, void* s
   if (t->cfg.kind != CH_SINGLE) return fail(CH_EINVAL, "erase is only defined for single-value tables");
   if (n && (!keys || !erased)) return fail(CH_EINVAL, "null buffer");
   Ordered o(t, stream);
+  if (use_staged(t, n) && g_staged_erase) {
+    Scratch sc(o.s);
+    void* p = sc.get(staged_scratch_bytes(t->T, n, false));
+    if (!p) return o.done(fail(CH_ENOMEM, "scratch allocation failed"));
+    return o.done(staged_erase(o.lc, t->T, t->ts, keys, n, erased, p));
+  }
   return o.done(single_lookup(o.lc, t->T, t->ts, keys, n, nullptr, erased, nullptr, nullptr, nullptr, 2));
 }
 

@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(256, CH_AB_PROBE_MINB) k_lookup(TableRef T, co
       if (win_out) stage_out(win_out, s_win, cs);
       if (vals_out) stage_out(vals_out, s_vals, cs);
     } else {
-      stage_out(flag, s_flag, cs);
+      stage_out_ix(flag, s_flag, cs, out_idx);  // erase (staged.cu passes out_idx for its deferred keys)
     }
   }
   const long long v[5] = {ops, att, win, occ, tomb};

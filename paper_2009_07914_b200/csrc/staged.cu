@@ -1146,6 +1146,11 @@ __device__ __forceinline__ uint32_t flag_mask8(uint32_t f0, uint32_t f1) {
   return (f0 >> 4) * 0x00204081u + f1 * 0x00204081u;
 }
 
+// ERASE: the same pass retires the keys it finds (single_table.py:338-351): a shared-memory CAS
+// of the key's word to the tombstone, the erased flag in res_flag, and the region written back
+// when anything was retired.  Keys whose window crosses the region end go to the COPS erase
+// (after every region is written back: the halo belongs to the next region's CTA).
+template <bool ERASE>
 __global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, const uint32_t* __restrict__ keys,
                                                        const uint16_t* __restrict__ los,
                                                        uint32_t* __restrict__ res_val, uint8_t* __restrict__ res_flag,
@@ -1159,6 +1164,7 @@ __global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, cons
   uint32_t* qlo = qi + LQ_CAP;
   __shared__ DeferBuf<false, DBUF_B> B;
   __shared__ uint32_t s_qn;
+  __shared__ int s_dirty;
   __shared__ __align__(8) uint64_t bar;
   const uint32_t f = blockIdx.x;
   uint64_t k0;
@@ -1178,6 +1184,7 @@ __global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, cons
   if (threadIdx.x == 0) {
     B.n = 0;
     s_qn = 0;
+    s_dirty = 0;
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, (len + HALO) * 8u);
     bulk_load(tile, slots + rbase, len * 8u, &bar);
@@ -1187,7 +1194,7 @@ __global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, cons
   const uint32_t e = (uint32_t)T.e, t = (uint32_t)T.t;
   const uint32_t gm = ~((uint32_t)g - 1u), ug = (uint32_t)g;
   const uint32_t lane = threadIdx.x & 31u;
-  uint32_t att = 0, ndef = 0, nsent = 0;
+  uint32_t att = 0, ndef = 0, nsent = 0, nerased = 0;
   const uint32_t* const tw = reinterpret_cast<const uint32_t*>(tile);
   const uint32_t* const kp = keys + k0;
   const uint16_t* const lp = los + k0;
@@ -1253,8 +1260,21 @@ __global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, cons
       return false;
     }
     const bool hit = c == k;
-    rvp[i] = hit ? tw[s2 + 1] : 0u;
-    rfp[i] = (uint8_t)hit;
+    if (ERASE) {
+      bool erased = false;
+      if (hit) {  // retire: key word -> tombstone, value zeroed (layout.py:231)
+        const unsigned long long w = ((unsigned long long)tw[s2 + 1] << 32) | c;
+        erased = atomicCAS(reinterpret_cast<unsigned long long*>(tile) + (lo + o), w, (unsigned long long)t) == w;
+        if (erased) {
+          nerased += 1;
+          s_dirty = 1;
+        }
+      }
+      rfp[i] = (uint8_t)erased;
+    } else {
+      rvp[i] = hit ? tw[s2 + 1] : 0u;
+      rfp[i] = (uint8_t)hit;
+    }
     att += (o & gm) + ug;  // chunk_end(o, g)
     return false;
   };
@@ -1277,9 +1297,12 @@ __global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, cons
       const uint32_t i = base + x * LQT + threadIdx.x;
       if (i < m) {
         if (k[x] == e || k[x] == t) {  // sentinels are never stored (single_table.py:391-393)
-          rvp[i] = 0;
+          if (!ERASE) rvp[i] = 0;
           rfp[i] = 0;
           nsent += 1;
+        } else if (ERASE && lo[x] + WINDOW > len) {  // window 0 reaches into the next region
+          defer_push(B, DB, k[x], 0u, k0u + i, 0u);
+          ndef += 1;
         } else {
           open[x] = step(k[x], fp7(k[x]) * 0x01010101u, lo[x], i, o[x]);
         }
@@ -1319,11 +1342,18 @@ __global__ void __launch_bounds__(LQT, 2) k_st_lookup_q(TableRef T, Part P, cons
     }
   }
   defer_flush(B, DB, true);  // syncs
-  // every key of the region is either resolved (one op, one window unless a sentinel) or deferred
-  const long long ops = (threadIdx.x == 0 ? (long long)m : 0ll) - (long long)ndef;
-  const long long cv6[6] = {ops, (long long)att, ops - (long long)nsent, 0ll, 0ll, (long long)ndef};
+  if (ERASE && s_dirty) {  // the retired keys back to the table (the halo stays untouched)
+    fence_smem_to_async();
+    __syncthreads();
+    if (threadIdx.x == 0) bulk_store_wait(const_cast<uint64_t*>(slots) + rbase, tile, len * 8u);
+  }
+  // every key of the region is either resolved (one op, one window unless a sentinel) or deferred;
+  // erase counts no sentinel (single_table.py:338-351)
+  const long long ops = (threadIdx.x == 0 ? (long long)m : 0ll) - (long long)ndef - (ERASE ? (long long)nsent : 0ll);
+  const long long cv6[6] = {ops, (long long)att, ops - (ERASE ? 0ll : (long long)nsent), -(long long)nerased,
+                            (long long)nerased, (long long)ndef};
   long long* const dst[6] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
-                             &T.ctr->occupied, nullptr, (long long*)&T.ctr->deferred};
+                             &T.ctr->occupied, ERASE ? &T.ctr->tombstones : nullptr, (long long*)&T.ctr->deferred};
   cta_add<6>(cv6, dst);
 }
 constexpr size_t lookup_q_smem() { return (size_t)(ST_R + ST_HALO + TILE_PAD) * 8 + FP_BYTES + LQ_CAP * 12; }
@@ -2353,18 +2383,20 @@ static int st_probe(const Launch& lc, const TableRef& T, const StPlan& p, const 
     if (!g_insert_sg) st_timed_end(lc, e0);
     return cuda_check(cudaGetLastError(), "staged region insert");
   }
-  if (MODE == 1 && !R2 && !g_probe_v1) {  // uniform rounds + queue (k_st_lookup_q)
+  if ((MODE == 1 && !R2 && !g_probe_v1) || MODE == 2) {  // uniform rounds + queue (k_st_lookup_q)
     const size_t sm = lookup_q_smem();
-    int rc = st_smem(k_st_lookup_q, sm);
+    auto lq = MODE == 2 ? k_st_lookup_q<true> : k_st_lookup_q<false>;
+    int rc = st_smem(lq, sm);
     if (rc) return rc;
     st_timed(lc, &e0);
-    k_st_lookup_q<<<p.regions, LQT, sm, lc.stream>>>(T, r.part, r.k2, r.lo2, rv, rf, DB, g);
+    lq<<<p.regions, LQT, sm, lc.stream>>>(T, r.part, r.k2, r.lo2, rv, rf, DB, g);
     count_launch();
     st_timed_end(lc, e0);
     return cuda_check(cudaGetLastError(), "staged region lookup");
   }
-  const size_t sm = probe_smem<MODE, R2>();
-  auto kern = k_st_probe<MODE, R2>;
+  if constexpr (MODE == 2) return 0;  // (erase always takes the uniform-round pass above)
+  const size_t sm = probe_smem<MODE == 2 ? 1 : MODE, R2>();
+  auto kern = k_st_probe<MODE == 2 ? 1 : MODE, R2>;
   int rc = st_smem(kern, sm);
   if (rc) return rc;
   if (!R2) st_timed(lc, &e0);  // the dominant kernel of the staged schedule (bench.py roofline)
@@ -2445,6 +2477,31 @@ int staged_lookup(const Launch& lc, const TableRef& T, const TypeSel& ts, const 
   rest.max_blocks = g_fb_blocks * lc.sms;
   if ((rc = single_lookup(rest, T, ts, b.rd.k1, n, b.rv, b.rf, nullptr, nullptr, nullptr, 0))) return rc;
   return st_backward<true>(lc, p, b, n, b.rv, b.rf, (uint32_t*)vals_out, found);
+}
+
+// Bulk erase (single_table.py:338-351) on the staged schedule: the lookup partitions, the
+// region pass retiring what it finds (k_st_lookup_q<true>), the COPS erase for the deferred
+// keys, and the erased flags back through the status gathers.
+int staged_erase(const Launch& lc, const TableRef& T, const TypeSel& ts, const void* keys, uint64_t n,
+                 uint8_t* erased, void* scratch) {
+  const StPlan p = st_plan(T, n);
+  size_t total = 0;
+  StBufs b = st_carve(p, n, false, false, scratch, &total);
+  int rc = cuda_check(cudaMemsetAsync(b.dcount, 0, 16, lc.stream), "memset");
+  const DeferOut DA{b.ak, nullptr, b.ax, b.ao, b.dcount};
+  if (!rc)
+    rc = st_forward<0>(lc, T, p, b.r1, (const uint32_t*)keys, nullptr, nullptr, nullptr, n, nullptr, 0, 2, &DA);
+  if (rc) return rc;
+  if ((rc = st_probe<2, false>(lc, T, p, b.r1, nullptr, nullptr, nullptr, b.rf, DA, DA, ts.g))) return rc;
+  if ((rc = st_forward<2>(lc, T, p, b.rd, b.ak, b.ax, b.ao, nullptr, n, b.dcount, 1, 1))) return rc;
+  Launch rest = lc;
+  rest.timer = nullptr;
+  rest.n_dev = b.dcount;
+  rest.out_idx = b.rd.v1;
+  rest.o_start = b.rd.p1;
+  rest.max_blocks = g_fb_blocks * lc.sms;
+  if ((rc = single_lookup(rest, T, ts, b.rd.k1, n, nullptr, b.rf, nullptr, nullptr, nullptr, 2))) return rc;
+  return st_backward<false>(lc, p, b, n, nullptr, b.rf, nullptr, erased);
 }
 
 }  // namespace chb

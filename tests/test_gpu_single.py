@@ -761,3 +761,58 @@ def test_deferred_clear_semantics():
     f = f.cpu().numpy()
     assert f[: 1 << 21].all() and not f[1 << 21:].any()
     assert (v.cpu().numpy().view(np.uint32)[: 1 << 21] == vals[: 1 << 21].astype(np.uint32)).all()
+
+
+@pytest.mark.parametrize("rho", [0.9, 0.97])
+def test_staged_erase_matches_direct(rho):
+    """Bulk erase on the staged schedule (csrc/staged.cu k_st_lookup_q<true>: region pass retiring
+    by shared-memory CAS, COPS erase for the keys past window 0 or crossing the region end)
+    against the direct COPS erase on a cell-for-cell copy of the same table: erased flags, the
+    table afterwards (tombstones in the same cells), ops / attempts / windows / occupied /
+    tombstone deltas -- then in-batch duplicate erases (exactly one copy erases) and erasing
+    over existing tombstones."""
+    from paper_2009_07914_b200 import _lib
+    n = 1 << 20
+    rng = np.random.default_rng(int(rho * 100) + 5)
+    pool = rng.permutation(np.unique(rng.integers(1, (1 << 32) - 3, size=3 * n, dtype=np.uint64)))
+    present, absent = pool[:n], pool[n:2 * n]
+
+    def table():
+        return SingleValueHashTable(int(n / rho), layout="packed", key_bits=32, value_bits=32, group_width=8)
+
+    a, b = table(), table()
+    a.set_locality("staged")
+    a.insert_device(present, present ^ np.uint64(3))
+    ks, vs = a._dt.read_slots()
+    _lib.check(_lib.lib().ch_write_slots(b._dt.handle, ks.ctypes.data, vs.ctypes.data), "write slots")
+    b.set_locality("off")
+
+    def erase_both(keys):
+        res = []
+        for t in (a, b):
+            t.reset_probe_counters()
+            o0, t0 = t.occupied, t.tombstones
+            e = t.erase_device(keys).cpu().numpy()
+            c = t.probe_counters()
+            res.append((e, (c.ops, c.attempts, c.windows_visited, t.occupied - o0, t.tombstones - t0)))
+        return res
+
+    q = rng.permutation(np.concatenate([present[::3], absent[: n // 4], np.array([0xFFFFFFFF], dtype=np.uint64)]))
+    (ea, ca), (eb, cb) = erase_both(q)
+    assert np.array_equal(ea, eb) and ca == cb
+    assert ea.sum() == present[::3].size
+    assert np.array_equal(a._dt.read_slots()[0], b._dt.read_slots()[0])
+    # erasing next to tombstones, and in-batch duplicates (one copy of each key erases)
+    q2 = rng.permutation(np.concatenate([present[1::3], present[1::3][:5000], present[::3][:1000]]))
+    (ea, ca), (eb, cb) = erase_both(q2)
+    for e in (ea, eb):
+        got = {}
+        for k, f in zip(q2.tolist(), e.tolist()):
+            got[k] = got.get(k, 0) + f
+        assert all(got[k] == 1 for k in present[1::3].tolist())
+        assert all(got[k] == 0 for k in present[::3][:1000].tolist())
+    assert ca[3:] == cb[3:]
+    assert np.array_equal(a._dt.read_slots()[0], b._dt.read_slots()[0])
+    v, f = a.retrieve_device(present)
+    f = f.cpu().numpy().astype(bool)
+    assert (f == (np.arange(n) % 3 == 2)).all()
