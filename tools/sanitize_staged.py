@@ -29,3 +29,10 @@ st2 = t2.insert_device(k2, k2).cpu().numpy()
 v2, f2 = t2.retrieve_device(k2)
 torch.cuda.synchronize()
 print("skew", (st2 == 0).all(), f2.cpu().numpy().all(), (v2.cpu().numpy().view(np.uint32) == k2.astype(np.uint32)).all())
+
+# staged bulk erase (retiring region pass, region write-back, deferred COPS erase), with duplicates
+q = np.concatenate([keys[::2], keys[::2][:1000]])
+er = t.erase_device(q).cpu().numpy()
+v3, f3 = t.retrieve_device(keys)
+torch.cuda.synchronize()
+print("erase", int(er.sum()) == keys[::2].size, not f3.cpu().numpy()[::2].any(), f3.cpu().numpy()[1::2].all())
