@@ -1796,7 +1796,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
 #pragma unroll
   for (int u = 0; u < (int)SG_PER; ++u) {
     const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
-    kk[u] = i < m ? __ldcs(kp + i) : 0u;
+    kk[u] = i < m ? kp[i] : 0u;  // (kept in L2: the placement reads the keys again)
     ks0[u] = i < m ? (uint32_t)__ldcs(lp + i) : 0u;
     if (i < m && (threadIdx.x & 31u) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + i));
   }
@@ -1952,11 +1952,13 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   };
 #pragma unroll
   for (int g4 = 0; g4 < (int)SG_PER; g4 += 4) {
-    uint32_t vv[4];
+    uint32_t vv[4], kr[4];  // values and keys again (L2): no key registers live through the scan
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
       const int u = g4 + x;
-      vv[x] = ((ks[u] >> 28) & 7u) == SG_PART ? __ldcs(vp + threadIdx.x + (uint32_t)u * SGT) : 0u;
+      const bool part = ((ks[u] >> 28) & 7u) == SG_PART;
+      vv[x] = part ? __ldcs(vp + threadIdx.x + (uint32_t)u * SGT) : 0u;
+      kr[x] = part ? __ldcs(kp + threadIdx.x + (uint32_t)u * SGT) : 0u;
     }
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
@@ -1966,11 +1968,11 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       if (r >= (w >> 16)) {  // past what window 0 holds for this group: resume at window 1 (a
         // window crossing the region end: at window 0, its next-region slots are unexamined)
         ks[u] = (lo + WINDOW > len ? SG_DEFA : SG_DEFB) << 28 | 1u << 27 | lo << 14;
-        cq_push(kk[u], lo, 63u);  // must not equal a placed key of its group
+        cq_push(kr[x], lo, 63u);  // must not equal a placed key of its group
         continue;
       }
       const uint32_t sl = slot_of((w & 0xFFFFu) + r);
-      tile[sl] = (uint64_t)vv[x] << 32 | kk[u];
+      tile[sl] = (uint64_t)vv[x] << 32 | kr[x];
       occn += 1;
       att += ((sl - lo) & gm) + ug;
     }
@@ -2012,7 +2014,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       nexc += 1;
       att += ((ks[u] & 0x3FFFu) & gm) + ug;
     } else {
-      defer_push(cls == SG_DEFA ? BA : B, cls == SG_DEFA ? DA : DB, kk[u], vp[i], k0u + i,
+      defer_push(cls == SG_DEFA ? BA : B, cls == SG_DEFA ? DA : DB, kp[i], vp[i], k0u + i,
                  cls == SG_DEFA ? 0u : WINDOW);
       ndef += 1;
     }
