@@ -1791,14 +1791,18 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     }
   };
   // the region's keys and window starts (coalesced), in flight while the tile lands; the
-  // values (needed at the placement) are prefetched into L2
+  // values (needed at the placement) are prefetched into L2 by one bulk prefetch
+  if (threadIdx.x == 0 && m) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(vp) & ~(uintptr_t)15;
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(vp + m) + 15) & ~(uintptr_t)15;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+  }
   uint32_t kk[SG_PER], ks0[SG_PER];
 #pragma unroll
   for (int u = 0; u < (int)SG_PER; ++u) {
     const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
     kk[u] = i < m ? kp[i] : 0u;  // (kept in L2: the placement reads the keys again)
     ks0[u] = i < m ? (uint32_t)__ldcs(lp + i) : 0u;
-    if (i < m && (threadIdx.x & 31u) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + i));
   }
   __syncthreads();  // zeroed, mbarrier initialised
   // any occupied cell in the tile?  (16-byte reads of the key words; the common case -- a
