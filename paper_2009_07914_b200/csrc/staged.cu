@@ -113,6 +113,13 @@ __device__ __forceinline__ void bulk_store_wait(void* dst, const void* src, uint
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void fence_smem_to_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// bulk prefetch of [p, p + bytes) into L2 (one thread; 16-byte granules, size < 2^32)
+__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
+  if (!bytes) return;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~(uintptr_t)15;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+}
 
 // ------------------------------------------------------------- count
 // Region histogram of the batch (dynamic shared memory, one counter per region).
@@ -189,6 +196,7 @@ struct Part {
   unsigned long long* ovf2;  // level-2 overflow results: positions ovf2_base + ...
   uint32_t ovf2_base;
   DeferOut da;               // level-2 overflow keys -> list A (resume at window 0)
+  uint32_t pfd;              // level 1, a CTA per tile: prefetch tile t + pfd into L2 (0: off)
 };
 
 // tstart from per-super-region element counts (one CTA of PT threads)
@@ -384,9 +392,25 @@ __global__ void __launch_bounds__(PT, (L == 2 && NPAY >= 1) ? CH_AB_L2P_MINB : (
   uint32_t* const cursor = L == 1 ? P.cur1 : P.cur2;
   // persistent CTAs (a gated redo exits in one wave)
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (L == 1 && P.pfd && threadIdx.x == 0) {  // the tile a CTA starts one wave from now, into L2
+      const uint64_t q0 = (uint64_t)(t + P.pfd) * PTILE;
+      if (q0 < n) {
+        const uint64_t cn = (n - q0) < PTILE ? (n - q0) : PTILE;
+        l2_prefetch(kin + q0, cn * 4);
+        if (VALS) l2_prefetch(vin + q0, cn * 4);
+      }
+    }
     if (L == 2) tile_super(t, P, supers, s_sup);
     TileGeo g;
     if (!tile_geo<L>(t, n, P, s_sup, g)) break;  // tiles past the end are past it for every later t
+    if (L == 2 && P.pfd && threadIdx.x == 0) {  // the same super-region's tile one wave ahead
+      const uint64_t q0 = g.pos0 + (uint64_t)P.pfd * PTILE, end = (uint64_t)s_sup[2] + s_sup[3];
+      if (q0 < end) {
+        const uint64_t cn = (end - q0) < PTILE ? (end - q0) : PTILE;
+        l2_prefetch(kin + q0, cn * 4);
+        if (VALS) l2_prefetch(vin + q0, cn * 4);
+      }
+    }
     hist[threadIdx.x] = 0;  // PBINS == PT
     // d: bucket | rank << 16 (one register per item); level 2 with payloads keeps
     // bucket | window start << 16 and the rank apart (measured faster than staging the
@@ -1792,11 +1816,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   };
   // the region's keys and window starts (coalesced), in flight while the tile lands; the
   // values (needed at the placement) are prefetched into L2 by one bulk prefetch
-  if (threadIdx.x == 0 && m) {
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(vp) & ~(uintptr_t)15;
-    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(vp + m) + 15) & ~(uintptr_t)15;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
-  }
+  if (threadIdx.x == 0) l2_prefetch(vp, (size_t)m * 4);
   uint32_t kk[SG_PER], ks0[SG_PER];
 #pragma unroll
   for (int u = 0; u < (int)SG_PER; ++u) {
@@ -2199,6 +2219,12 @@ static int g_fb_blocks = [] {
   return v > 0 ? v : 0;
 }();
 
+// CH_SPLIT_PFD=0: level-1 partition CTAs do not prefetch the tile one wave ahead
+static bool g_split_pfd = [] {
+  const char* e = getenv("CH_SPLIT_PFD");
+  return !(e && e[0] == '0');
+}();
+
 // CH_INSERT_SG=0: inserts without the sorted-greedy placement pass (k_st_insert_sg)
 static bool g_insert_sg = [] {
   const char* e = getenv("CH_INSERT_SG");
@@ -2311,6 +2337,11 @@ static int st_forward(const Launch& lc, const TableRef& T, const StPlan& p, Roun
     if (rc) return rc;
     Part L1 = P;
     L1.cr = 0;
+    if (g_split_pfd && g1 == t1) {  // one CTA per tile: prefetch a resident wave ahead
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k1f, PT, sm1);
+      L1.pfd = (uint32_t)(lc.sms * (occ > 0 ? occ : 1));
+    }
     k1f<<<g1, PT, sm1, lc.stream>>>(T, n, L1, p.supers, t1, k, v, q, w, r.k1, r.v1, r.p1, r.r1, nullptr, r.inv1,
                                      r.th1, r.tg1, p.supers, n_dev, wj, r.bid1);
     count_launch();
@@ -2326,7 +2357,13 @@ static int st_forward(const Launch& lc, const TableRef& T, const StPlan& p, Roun
     if ((rc = count_mode_l1(P, levels == 2))) return rc;
   }
   if (levels == 2) {
-    k2f<<<g2, PT, sm2, lc.stream>>>(T, n, P, p.supers, t2, r.k1, r.v1, r.p1, r.r1, r.k2, r.v2, r.p2, r.r2, r.lo2,
+    Part P2 = P;
+    if (g_split_pfd && !n_dev && NPAY <= 1) {  // one CTA per tile: prefetch a resident wave ahead
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k2f, PT, sm2);
+      P2.pfd = (uint32_t)(lc.sms * (occ > 0 ? occ : 1));
+    }
+    k2f<<<g2, PT, sm2, lc.stream>>>(T, n, P2, p.supers, t2, r.k1, r.v1, r.p1, r.r1, r.k2, r.v2, r.p2, r.r2, r.lo2,
                                      r.inv2, r.th2, r.tg2, 256, n_dev, wj, r.bid2);
     count_launch();
   }
