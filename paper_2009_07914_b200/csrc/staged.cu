@@ -1875,6 +1875,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
   // (b) exclusions (region order, no side effects yet); participants take a rank in their group.
   // Key state ks: class << 28 | over-placed flag << 27 | lo << 14 | rank (or probe offset).
   uint32_t ks[SG_PER];
+  uint32_t special = 0;  // bit u: item u ends as anything but placed / absent (phase (f) looks at those only)
 #pragma unroll
   for (int u = 0; u < (int)SG_PER; ++u) {
     const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
@@ -1883,6 +1884,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     const uint32_t k = kk[u], lo = ks0[u];
     if (k == e || k == t) {  // sentinels are never stored (single_table.py:369-370)
       ks[u] = SG_INV << 28;
+      special |= 1u << u;
       continue;
     }
     // a window crossing the region end takes part with its own-region slots (they come first in
@@ -1896,11 +1898,13 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       }
       if (o < span && tw[2 * (lo + o)] == k) {
         ks[u] = SG_DUP << 28 | lo << 14 | o;
+        special |= 1u << u;
         continue;
       }
     }
     if (occ_any && fidx(lo) == fidx(lo + span)) {  // neither the key nor a free cell here
       ks[u] = (span < WINDOW ? SG_DEFA : SG_DEFB) << 28 | lo << 14;  // the rest of window 0 / window 1
+      special |= 1u << u;
       continue;
     }
     // the rank in the group (count, bits 0..15) and one bit of the key's hash ORed into the
@@ -1992,6 +1996,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       if (r >= (w >> 16)) {  // past what window 0 holds for this group: resume at window 1 (a
         // window crossing the region end: at window 0, its next-region slots are unexamined)
         ks[u] = (lo + WINDOW > len ? SG_DEFA : SG_DEFB) << 28 | 1u << 27 | lo << 14;
+        special |= 1u << u;
         cq_push(kr[x], lo, 63u);  // must not equal a placed key of its group
         continue;
       }
@@ -2021,15 +2026,13 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     if (threadIdx.x == 0) redo[atomicAdd(n_redo, 1ull)] = f;
     return;
   }
-  // (f) results: statuses, deferrals, counters
+  // (f) results: statuses, deferrals, counters (placed keys were counted at the placement)
 #pragma unroll
   for (int u = 0; u < (int)SG_PER; ++u) {
+    if (!((special >> u) & 1u)) continue;
     const uint32_t cls = (ks[u] >> 28) & 7u;
-    if (cls == SG_NONE) continue;
     const uint32_t i = threadIdx.x + (uint32_t)u * SGT;
-    if (cls == SG_PART) {
-      continue;  // counted at the placement
-    } else if (cls == SG_INV) {
+    if (cls == SG_INV) {
       stp[i] = ST_INVALID;
       nexc += 1;
       nsent += 1;
