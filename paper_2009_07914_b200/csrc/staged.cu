@@ -1795,7 +1795,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       bulk_load(tile, slots + rbase, len * 8u, &bar);
     }
   }
-  for (uint32_t w = threadIdx.x; w < ST_R; w += SGT) cs[w] = 0;
+  for (uint32_t q = threadIdx.x; q < ST_R / 4; q += SGT) reinterpret_cast<uint4*>(cs)[q] = make_uint4(0u, 0u, 0u, 0u);
   const uint32_t e = (uint32_t)T.e, t = (uint32_t)T.t;
   const uint32_t gm = ~((uint32_t)g - 1u), ug = (uint32_t)g;
   const uint32_t* const kp = keys + k0;
