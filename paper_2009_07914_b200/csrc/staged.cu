@@ -1657,6 +1657,10 @@ constexpr uint32_t SG_PER = SG_MAXK / SGT;    // keys per thread (region order)
 constexpr uint32_t SG_LPT = (ST_R + SGT - 1) / SGT;  // window starts per thread (11)
 constexpr uint32_t SG_DBUF = 192;             // deferrals buffered per region
 constexpr uint32_t SG_CQ = 512;               // duplicate-check queue (~6% of the keys)
+#ifndef CH_AB_SG_PB
+#define CH_AB_SG_PB 4
+#endif
+constexpr int SG_PB = CH_AB_SG_PB;             // values / keys read per placement batch
 static_assert(SG_MAXK % SGT == 0 && SG_PER <= 12, "sorted pass geometry");
 
 template <int NT>
@@ -1979,17 +1983,17 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     return 32 * lo_w + __ffs(fb) - 1;
   };
 #pragma unroll
-  for (int g4 = 0; g4 < (int)SG_PER; g4 += 4) {
-    uint32_t vv[4], kr[4];  // values and keys again (L2): no key registers live through the scan
+  for (int g4 = 0; g4 < (int)SG_PER; g4 += SG_PB) {
+    uint32_t vv[SG_PB], kr[SG_PB];  // values and keys again (L2): no key registers live through the scan
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
+    for (int x = 0; x < SG_PB; ++x) {
       const int u = g4 + x;
       const bool part = ((ks[u] >> 28) & 7u) == SG_PART;
       vv[x] = part ? __ldcs(vp + threadIdx.x + (uint32_t)u * SGT) : 0u;
       kr[x] = part ? __ldcs(kp + threadIdx.x + (uint32_t)u * SGT) : 0u;
     }
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
+    for (int x = 0; x < SG_PB; ++x) {
       const int u = g4 + x;
       if (((ks[u] >> 28) & 7u) != SG_PART) continue;
       const uint32_t lo = (ks[u] >> 14) & 0x1FFFu, r = ks[u] & 0x3FFFu, w = cs[lo];
