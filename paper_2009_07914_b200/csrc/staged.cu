@@ -113,6 +113,14 @@ __device__ __forceinline__ void bulk_store_wait(void* dst, const void* src, uint
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void fence_smem_to_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// shared -> global bulk copy issued now, its shared-memory read awaited later (bulk_read_wait)
+__device__ __forceinline__ void bulk_store_issue(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_read_wait() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 // bulk prefetch of [p, p + bytes) into L2 (one thread; 16-byte granules, size < 2^32)
 __device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
   if (!bytes) return;
@@ -816,6 +824,35 @@ __device__ __forceinline__ void defer_flush(DeferBuf<VALS, CAP>& B, const DeferO
     D.o[gb + i] = B.o[i];
   }
   __syncthreads();
+}
+
+// both deferral buffers of a region at once (one pair of barriers instead of two)
+template <bool VALS, uint32_t CAP>
+__device__ __forceinline__ void defer_flush2(DeferBuf<VALS, CAP>& B1, const DeferOut& D1, DeferBuf<VALS, CAP>& B2,
+                                             const DeferOut& D2) {
+  __syncthreads();
+  const uint32_t n1 = B1.n < CAP ? B1.n : CAP, n2 = B2.n < CAP ? B2.n : CAP;
+  __syncthreads();  // everyone has read the counts
+  if (!(n1 | n2)) return;
+  if (threadIdx.x == 0) {
+    if (n1) B1.gb = atomicAdd(D1.count, (unsigned long long)n1);
+    if (n2) B2.gb = atomicAdd(D2.count, (unsigned long long)n2);
+    B1.n = 0;
+    B2.n = 0;
+  }
+  __syncthreads();
+  const unsigned long long g1 = B1.gb, g2 = B2.gb;
+  for (uint32_t i = threadIdx.x; i < n1 + n2; i += blockDim.x) {
+    const bool a = i < n1;
+    DeferBuf<VALS, CAP>& Bx = a ? B1 : B2;
+    const DeferOut& Dx = a ? D1 : D2;
+    const uint32_t j = a ? i : i - n1;
+    const unsigned long long gd = (a ? g1 : g2) + j;
+    Dx.k[gd] = Bx.k[j];
+    if (VALS) Dx.v[gd] = Bx.v[j];
+    Dx.x[gd] = Bx.x[j];
+    Dx.o[gd] = Bx.o[j];
+  }
 }
 
 __device__ __forceinline__ uint32_t lds32(const uint32_t* p) {
@@ -2010,6 +2047,7 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       att += ((sl - lo) & gm) + ug;
     }
   }
+  fence_smem_to_async();  // the placed tile, for the bulk store issued after the duplicate check
   __syncthreads();
   // (e) in-batch duplicates.  Copies of a key share a window start, so they are in one group.  In
   // (b) every participant ORs one bit of its key hash into its group's 16-bit signature; a key whose
@@ -2030,6 +2068,8 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
     if (threadIdx.x == 0) redo[atomicAdd(n_redo, 1ull)] = f;
     return;
   }
+  // the region is final: its write-back runs while the results and deferrals are written
+  if (threadIdx.x == 0) bulk_store_issue(slots + rbase, tile, len * 8u);
   // (f) results: statuses, deferrals, counters (placed keys were counted at the placement)
 #pragma unroll
   for (int u = 0; u < (int)SG_PER; ++u) {
@@ -2050,11 +2090,8 @@ __global__ void __launch_bounds__(SGT, 2) k_st_insert_sg(TableRef T, Part P, con
       ndef += 1;
     }
   }
-  defer_flush(B, DB, true);  // syncs
-  defer_flush(BA, DA, true);
-  fence_smem_to_async();
-  __syncthreads();
-  if (threadIdx.x == 0) bulk_store_wait(slots + rbase, tile, len * 8u);
+  defer_flush2(B, DB, BA, DA);  // syncs
+  if (threadIdx.x == 0) bulk_read_wait();  // the tile must stay until the store has read it
   const long long ops = (threadIdx.x == 0 ? (long long)m : 0ll) - (long long)ndef - (long long)nsent;
   const long long cv6[6] = {ops, (long long)att, ops, (long long)occn, (long long)nexc, (long long)ndef};
   long long* const dst[6] = {(long long*)&T.ctr->ops, (long long*)&T.ctr->attempts, (long long*)&T.ctr->windows,
